@@ -1,0 +1,256 @@
+"""Galerkin operators of a single patch or a conforming multi-patch domain.
+
+Test infrastructure only (see oracle/__init__.py).
+
+Definitions written out as sparse matrix products over the Gauss points:
+  M_ij = sum_q w_q |J(q)| B_i(q) B_j(q)
+  K_ij = sum_q w_q |J(q)| omega^2 grad B_i(q) . grad B_j(q)     (weak form of P:57)
+  elastic K_(i,a),(j,b) = sum_q w|J| [lam d_aB_i d_bB_j + mu d_bB_i d_aB_j
+                                       + mu delta_ab grad B_i . grad B_j]
+with grad B = J^{-T} grad_xi B (isoparametric push-forward).
+The quadrature rule is (p+1) Gauss points per element per direction
+(the rule defines M and K on deformed maps)."""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import splines
+
+
+def tables_1d(p: int, n: int):
+    """Basis values / derivatives at the 1D Gauss points: (B, dB, w), B is (n(p+1), m)."""
+    t = splines.open_uniform_knots(p, n)
+    x, w = splines.quadrature_1d(p, n)
+    return splines.basis(t, p, x), splines.basis_deriv(t, p, x), w
+
+
+def _kron_all(mats):
+    """kron(..., kron(A_z, kron(A_y, A_x))) so that the x index is fastest
+    (co-lexicographic order).  mats = [A_x, A_y(, A_z)]."""
+    out = sp.csr_matrix(mats[0])
+    for A in mats[1:]:
+        out = sp.kron(sp.csr_matrix(A), out, format="csr")
+    return out
+
+
+class PatchQuad:
+    """Tensor-product quadrature data of one patch: basis matrices mapping the
+    m^d control coefficients to the (n(p+1))^d Gauss points, Jacobians, weights."""
+
+    def __init__(self, ctrl: np.ndarray, p: int, n: int, dim: int):
+        B1, dB1, w1 = tables_1d(p, n)
+        self.p, self.n, self.dim, self.m = p, n, dim, n + p
+        self.B = _kron_all([B1] * dim)
+        self.D = []  # parametric derivative matrices, D[c] = d/dxi_c
+        for c in range(dim):
+            mats = [dB1 if a == c else B1 for a in range(dim)]
+            self.D.append(_kron_all(mats))
+        w = w1
+        for _ in range(dim - 1):
+            w = np.kron(w1, w)
+        self.w = w
+        # J[q, a, b] = dF_a/dxi_b = sum_i C_i[a] dB_i/dxi_b
+        J = np.empty((self.B.shape[0], dim, dim))
+        for a in range(dim):
+            for b in range(dim):
+                J[:, a, b] = self.D[b] @ ctrl[:, a]
+        self.J = J
+        self.detJ = np.linalg.det(J)
+        self.Jinv = np.linalg.inv(J)
+        # physical derivative matrices: d_a B = sum_c Jinv[c, a] d_xi_c B
+        self.PD = []
+        for a in range(dim):
+            acc = None
+            for c in range(dim):
+                term = sp.diags(self.Jinv[:, c, a]) @ self.D[c]
+                acc = term if acc is None else acc + term
+            self.PD.append(sp.csr_matrix(acc))
+
+    def min_detJ(self) -> float:
+        return float(self.detJ.min())
+
+
+def patch_operators(ctrl, p, n, dim, ncomp=1, omega=1.0, lam=1.0, mu=1.0, density=1.0):
+    """Unreduced (all m^d control points) M and K of one patch.
+
+    ncomp = 1: scalar wave; ncomp = dim: linear elasticity, component-major
+    unknown ordering [u_x (all points), u_y, (u_z)].  Raises ValueError when
+    |J| <= 0 at a Gauss point (Assumption P:699-701)."""
+    Q = PatchQuad(ctrl, p, n, dim)
+    if Q.min_detJ() <= 0.0:
+        raise ValueError("non-positive Jacobian determinant")
+    W = sp.diags(Q.w * Q.detJ)
+    M = sp.csr_matrix(Q.B.T @ W @ Q.B)
+    if ncomp == 1:
+        K = None
+        for a in range(dim):
+            t = Q.PD[a].T @ W @ Q.PD[a]
+            K = t if K is None else K + t
+        K = sp.csr_matrix(omega ** 2 * K)
+        return M, K
+    assert ncomp == dim
+    lap = None
+    for f in range(dim):
+        t = Q.PD[f].T @ W @ Q.PD[f]
+        lap = t if lap is None else lap + t
+    blocks = [[None] * dim for _ in range(dim)]
+    for a in range(dim):
+        for b in range(dim):
+            blk = lam * (Q.PD[a].T @ W @ Q.PD[b]) + mu * (Q.PD[b].T @ W @ Q.PD[a])
+            if a == b:
+                blk = blk + mu * lap
+            blocks[a][b] = blk
+    K = sp.csr_matrix(sp.bmat(blocks))
+    Mel = sp.csr_matrix(sp.block_diag([density * M] * dim))
+    return Mel, K
+
+
+def interior_mask(m: int, dim: int) -> np.ndarray:
+    """Free (non-boundary) control points of a single patch, co-lex order:
+    homogeneous Dirichlet on every face removes index 0 and m-1."""
+    idx = np.indices((m,) * dim).reshape(dim, -1)[::-1]
+    return np.all((idx > 0) & (idx < m - 1), axis=0)
+
+
+class Discretization:
+    """Reduced (free-DoF) operators of a single- or multi-patch problem.
+
+    Multi-patch gluing: the global index map G^(r) identifies two
+    local functions iff they coincide on the interface, which for conforming
+    patches with matching knot vectors means coincident control points; a
+    patch face is an interface iff its control points match another patch's
+    face.  A global function is Dirichlet iff any of its local copies lies on
+    a face that is not an interface (homogeneous BC on the outer boundary).
+
+    Attributes
+      M, K          free-DoF matrices (scipy CSR), scalar or component-major
+      nfree         number of free scalar DoFs (per component)
+      local_of      list over free DoFs of (patch, local control index) (first copy)
+      G             per patch: array local index -> global index (or -1 if Dirichlet)
+    """
+
+    def __init__(self, patches, p, n, dim, ncomp=1, **mat):
+        self.p, self.n, self.dim, self.ncomp = p, n, dim, ncomp
+        m = n + p
+        self.m = m
+        npatch = len(patches)
+        ctrls = [c for _, c in patches]
+        # --- faces and interface detection --------------------------------
+        idx = np.indices((m,) * dim).reshape(dim, -1)[::-1]
+        faces = {}
+        for r in range(npatch):
+            for a in range(dim):
+                for side in (0, m - 1):
+                    sel = np.nonzero(idx[a] == side)[0]
+                    key = frozenset(map(tuple, ctrls[r][sel]))
+                    faces[(r, a, side)] = (sel, key)
+        is_iface = {}
+        for f, (sel, key) in faces.items():
+            is_iface[f] = any(g != f and g[0] != f[0] and k2 == key
+                              for g, (s2, k2) in faces.items())
+        # --- global numbering by coincident control points -----------------
+        coord_id = {}
+        glob_of = []  # per patch: local -> global (all points, incl. Dirichlet)
+        for r in range(npatch):
+            gl = np.empty(m ** dim, dtype=np.int64)
+            for i, pt in enumerate(map(tuple, ctrls[r])):
+                if pt not in coord_id:
+                    coord_id[pt] = len(coord_id)
+                gl[i] = coord_id[pt]
+            glob_of.append(gl)
+        nglob = len(coord_id)
+        dirichlet = np.zeros(nglob, dtype=bool)
+        for (r, a, side), (sel, _) in faces.items():
+            if not is_iface[(r, a, side)]:
+                dirichlet[glob_of[r][sel]] = True
+        free_ids = np.nonzero(~dirichlet)[0]
+        # canonical order of free DoFs: by (patch, local index) of first copy
+        first = {}
+        for r in range(npatch):
+            for i, g in enumerate(glob_of[r]):
+                if not dirichlet[g] and g not in first:
+                    first[g] = (r, i)
+        order = sorted(first.keys(), key=lambda g: first[g])
+        renum = -np.ones(nglob, dtype=np.int64)
+        renum[np.array(order, dtype=np.int64)] = np.arange(len(order))
+        self.nfree = len(order)
+        assert self.nfree == len(free_ids)
+        self.local_of = [first[g] for g in order]
+        self.G = [renum[gl] for gl in glob_of]
+        self.nadj = np.bincount(np.concatenate([g[g >= 0] for g in self.G]),
+                                minlength=self.nfree).max() if self.nfree else 0
+        # --- assembly: scatter-sum of patch contributions -------
+        Mg = sp.csr_matrix((nglob * ncomp, nglob * ncomp))
+        Kg = sp.csr_matrix((nglob * ncomp, nglob * ncomp))
+        self.min_detJ = np.inf
+        for r in range(npatch):
+            Mr, Kr = patch_operators(ctrls[r], p, n, dim, ncomp, **mat)
+            self.min_detJ = min(self.min_detJ, PatchQuad(ctrls[r], p, n, dim).min_detJ())
+            rows = np.concatenate([glob_of[r] + c * nglob for c in range(ncomp)])
+            Pr = sp.csr_matrix((np.ones(rows.size), (rows, np.arange(rows.size))),
+                               shape=(nglob * ncomp, rows.size))
+            Mg = Mg + Pr @ Mr @ Pr.T
+            Kg = Kg + Pr @ Kr @ Pr.T
+        self.M_full, self.K_full = sp.csr_matrix(Mg), sp.csr_matrix(Kg)
+        sel = np.concatenate([np.array(order, dtype=np.int64) + c * nglob for c in range(ncomp)])
+        self.M = sp.csr_matrix(Mg[sel][:, sel])
+        self.K = sp.csr_matrix(Kg[sel][:, sel])
+        self.nglob = nglob
+        self._order = np.array(order, dtype=np.int64)
+
+    def restrict_local(self, per_patch_values):
+        """Free-DoF vector from per-patch control-point values (m^d, ncomp)
+        (first copy wins; conforming data agree on interfaces)."""
+        out = np.empty((self.ncomp, self.nfree))
+        for f, (r, i) in enumerate(self.local_of):
+            out[:, f] = per_patch_values[r][i]
+        return out.reshape(-1)
+
+
+def operator_rows(ctrl, p, n, dim, rows, omega=1.0):
+    """Rows of the unreduced scalar M and K of one patch, computed one by one
+    by local quadrature over the support elements of each row (same
+    definitions as patch_operators).  rows: control-point multi-indices
+    (x, y(, z)).  Returns dict row -> (cols(list of multi-index), Mvals, Kvals).
+
+    Used for full-size sampled checks; pinned against patch_operators."""
+    t = splines.open_uniform_knots(p, n)
+    xg, wg = splines.gauss_legendre(p + 1)
+    m = n + p
+    h = 1.0 / n
+    out = {}
+    for row in rows:
+        row = tuple(int(v) for v in row)
+        # elements whose support contains B_row: e_d in [row_d - p, row_d] ∩ [0, n)
+        ranges = [range(max(0, r - p), min(n, r + 1)) for r in row]
+        acc_M, acc_K = {}, {}
+        for elem in itertools.product(*ranges):
+            # Gauss points of this element
+            pts1 = [(e + 0.5) * h + 0.5 * h * xg for e in elem]
+            w1 = [0.5 * h * wg for _ in elem]
+            vals = [splines.basis(t, p, pts1[d]) for d in range(dim)]
+            ders = [splines.basis_deriv(t, p, pts1[d]) for d in range(dim)]
+            for qi in itertools.product(range(p + 1), repeat=dim):
+                wq = np.prod([w1[d][qi[d]] for d in range(dim)])
+                # local basis indices of this element: e_d .. e_d + p
+                loc = list(itertools.product(*[range(elem[d], elem[d] + p + 1) for d in range(dim)]))
+                Bv = np.array([np.prod([vals[d][qi[d], j[d]] for d in range(dim)]) for j in loc])
+                Dv = np.array([[np.prod([(ders if d == c else vals)[d][qi[d], j[d]] for d in range(dim)])
+                                for c in range(dim)] for j in loc])
+                lin = [j[0] + m * (j[1] + (m * j[2] if dim == 3 else 0)) for j in loc]
+                J = np.zeros((dim, dim))
+                for jj, L in enumerate(lin):
+                    J += np.outer(ctrl[L], Dv[jj])
+                det = np.linalg.det(J)
+                Ji = np.linalg.inv(J)
+                G = Ji @ Ji.T
+                me = loc.index(row)
+                for jj, j in enumerate(loc):
+                    acc_M[j] = acc_M.get(j, 0.0) + wq * det * Bv[me] * Bv[jj]
+                    acc_K[j] = acc_K.get(j, 0.0) + wq * det * omega ** 2 * (Dv[me] @ G @ Dv[jj])
+        cols = sorted(acc_M.keys(), key=lambda j: j[::-1])
+        out[row] = (cols, np.array([acc_M[c] for c in cols]), np.array([acc_K[c] for c in cols]))
+    return out

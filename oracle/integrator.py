@@ -1,0 +1,98 @@
+"""Explicit order-2k generalized-alpha integrator (§3-§4).
+
+Test infrastructure only (see oracle/__init__.py).
+
+State chain c_0 .. c_{3k-1}:  c_0 = U, c_1 = V, c_2 = A, c_{m} = L^{m-2}(A)
+(P:123).  Block j (1-based) owns disp = 3j-3, vel = 3j-2,
+acc = 3j-1.  Taylor predictor T_m(c) = sum_{i=0}^{3k-1-m} tau^i/i! c_{m+i}.
+
+One step (P:398-431 with the jump [[.]] = Delta of P:113; reading R1 =
+SURVEY.md §8c G1 for the K-term of blocks j < k; F = C = 0):
+  s_j  = T_disp(c)   (j < k)      s_k = c_{3k-3}
+  y_j  = M^{-1}(-K s_j)           (= T_acc + alpha_j P_j, P:424/428/429)
+  P_j  = (y_j - T_acc(c)) / alpha_j
+  c'_disp = T_disp + beta_j tau^2 P_j   c'_vel = T_vel + gamma_j tau P_j
+  c'_acc  = T_acc + P_j
+All k blocks read only old-step data.
+
+Initial chain (P:119-121, P:155-162 generalised, reading R3):
+  c_0 = U_0, c_1 = V_0, c_m = M^{-1}(-K c_{m-2}), m = 2 .. 3k-1."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from .params import scheme_params
+
+
+class DirectMassSolver:
+    """Sparse LU of M (SuperLU) plus one step of iterative refinement
+    x += M^{-1}(b - M x) reusing the factorisation."""
+
+    def __init__(self, M):
+        self.M = sp.csc_matrix(M)
+        self.lu = spla.splu(self.M)
+
+    def __call__(self, b):
+        b = np.asarray(b, dtype=np.float64)
+        if not np.any(b):
+            return np.zeros_like(b)
+        x = self.lu.solve(b)
+        x += self.lu.solve(b - self.M @ x)
+        return x
+
+
+def taylor(c, m: int, tau: float):
+    """T_m(c) = sum_{i=0}^{len(c)-1-m} tau^i / i! c_{m+i}."""
+    out = np.array(c[m], dtype=np.float64, copy=True)
+    for i in range(1, len(c) - m):
+        out = out + (tau ** i / math.factorial(i)) * c[m + i]
+    return out
+
+
+def initial_chain(u0, v0, k: int, solve, Kop):
+    """c_0 = U_0, c_1 = V_0, c_m = M^{-1}(-K c_{m-2}) for m = 2..3k-1."""
+    c = [np.array(u0, dtype=np.float64), np.array(v0, dtype=np.float64)]
+    for m in range(2, 3 * k):
+        c.append(solve(-(Kop @ c[m - 2])))
+    return c
+
+
+def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop):
+    """One explicit step of the order-2k scheme; returns the new chain."""
+    new = [None] * (3 * k)
+    for j in range(1, k + 1):
+        d, v, a = 3 * j - 3, 3 * j - 2, 3 * j - 1
+        Td, Tv, Ta = taylor(c, d, tau), taylor(c, v, tau), taylor(c, a, tau)
+        s = Td if j < k else c[d]
+        y = solve(-(Kop @ s))
+        P = (y - Ta) / alpha[j - 1]
+        new[d] = Td + beta[j - 1] * tau * tau * P
+        new[v] = Tv + gamma[j - 1] * tau * P
+        new[a] = Ta + P
+    return new
+
+
+class Integrator:
+    """Convenience driver: M, K (free-DoF sparse matrices), k, rho, dt."""
+
+    def __init__(self, M, K, k: int, rho: float, dt: float, param_set: int = 0, solver=None):
+        self.M, self.K = sp.csr_matrix(M), sp.csr_matrix(K)
+        self.k, self.dt = k, dt
+        self.alpha, self.beta, self.gamma, self.alpha_f = scheme_params(k, rho, param_set)
+        self.solve = solver if solver is not None else DirectMassSolver(self.M)
+
+    def init(self, u0, v0):
+        return initial_chain(u0, v0, self.k, self.solve, self.K)
+
+    def step(self, c):
+        return step(c, self.k, self.dt, self.alpha, self.beta, self.gamma, self.solve, self.K)
+
+    def run(self, u0, v0, nsteps: int, chain=None):
+        c = self.init(u0, v0) if chain is None else chain
+        for _ in range(nsteps):
+            c = self.step(c)
+        return c

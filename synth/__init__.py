@@ -1,0 +1,147 @@
+"""Seeded synthetic inputs shared by the oracle, the tests and bench.py.
+
+This module holds NO arithmetic of the method (no basis functions, no
+quadrature, no operators, no time stepping).  It only produces the inputs a
+user hands to the library: control-point nets, initial coefficient vectors and
+the configuration table of BASELINE.json.  Both the CPU oracle (`oracle/`) and
+the CUDA path (`paper_2102_11536_b200`) consume these arrays; neither imports
+the other.
+
+Recipe:
+  * control points sit at the Greville abscissae (xi_{i+1}+...+xi_{i+p})/p of
+    the open uniform knot vector, which makes the undeformed map the identity;
+  * patch-interior control points get independent uniform noise
+    U(-a*h, a*h) per coordinate, h = 1/n, from numpy PCG64(seed); points on a
+    patch boundary are never moved (keeps the map onto the square/cube and the
+    multi-patch interfaces conforming);
+  * initial displacement coefficients are the control-point interpolation of
+    u0(x) = sum_{m=1..8} a_m prod_d sin(m pi x_d), a_m ~ N(0,1)/m^2 (seeded),
+    v0 = 0.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "greville_1d", "control_net", "lshape_patches", "sine_modes", "eval_modes",
+    "sinpi_product", "CONFIGS", "config", "make_problem",
+]
+
+
+def greville_1d(p: int, n: int) -> np.ndarray:
+    """Greville abscissae of the open uniform knot vector with n elements, degree p.
+
+    The knot vector is {0^(p+1), 1/n, ..., (n-1)/n, 1^(p+1)} (PAPER.md:529-536,
+    uniform, maximal regularity PAPER.md:811).  Returned array has m = n+p
+    entries.  Used only to *place* control points (input generation)."""
+    inner = np.arange(1, n) / n
+    knots = np.concatenate([np.zeros(p + 1), inner, np.ones(p + 1)])
+    m = n + p
+    g = np.array([knots[i + 1:i + p + 1].sum() / p for i in range(m)])
+    g[0], g[-1] = 0.0, 1.0
+    return g
+
+
+def control_net(dim: int, p: int, n: int, noise: float = 0.0, seed: int = 0,
+                origin=None, rng: np.random.Generator | None = None) -> np.ndarray:
+    """Control-point net of one patch, shape (m**dim, dim), co-lexicographic
+    (x fastest), xyz interleaved per point.
+
+    noise = a: interior points (not on any patch face) move by U(-a h, a h) per
+    coordinate with h = 1/n.  origin shifts the patch (unit square/cube cell)."""
+    m = n + p
+    g = greville_1d(p, n)
+    axes = [g] * dim
+    grids = np.meshgrid(*axes[::-1], indexing="ij")[::-1]  # x fastest
+    pts = np.stack([gg.reshape(-1) for gg in grids], axis=1).astype(np.float64)
+    if origin is not None:
+        pts = pts + np.asarray(origin, dtype=np.float64)[None, :]
+    if noise > 0.0:
+        if rng is None:
+            rng = np.random.default_rng(seed)
+        idx = np.indices((m,) * dim).reshape(dim, -1)[::-1]  # idx[0] = x index
+        interior = np.all((idx > 0) & (idx < m - 1), axis=0)
+        h = 1.0 / n
+        delta = rng.uniform(-noise * h, noise * h, size=pts.shape)
+        pts[interior] += delta[interior]
+    return pts
+
+
+def lshape_patches(p: int, n: int, noise: float, seed: int):
+    """Three unit-square patches tiling the L-shape [0,2]^2 minus (1,2]^2.
+
+    Returns a list of (cell, ctrl) with cell = (cx, cy) the position of the
+    patch in the coarse patch grid: A=(0,0), B=(1,0), C=(0,1).  One PCG64
+    stream perturbs the patches in that order."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for cell in [(0, 0), (1, 0), (0, 1)]:
+        ctrl = control_net(2, p, n, noise=noise, origin=cell, rng=rng)
+        out.append((cell, ctrl))
+    return out
+
+
+def sine_modes(seed: int, nmodes: int = 8) -> np.ndarray:
+    """Amplitudes a_m ~ N(0,1)/m^2, m = 1..nmodes."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal(nmodes)
+    return a / (np.arange(1, nmodes + 1, dtype=np.float64) ** 2)
+
+
+def eval_modes(amp: np.ndarray, pts: np.ndarray) -> np.ndarray:
+    """u0(x) = sum_m a_m prod_d sin(m pi x_d) at the points pts (npts, dim)."""
+    u = np.zeros(pts.shape[0])
+    for mi, a in enumerate(amp, start=1):
+        u += a * np.prod(np.sin(mi * np.pi * pts), axis=1)
+    return u
+
+
+def sinpi_product(pts: np.ndarray) -> np.ndarray:
+    """u0 = prod_d sin(pi x_d) (BASELINE.json configs[0])."""
+    return np.prod(np.sin(np.pi * pts), axis=1)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configurations.  dt is NOT stored: it is
+# cfl_frac * sqrt(Theta_max(rho) / lambda_max), computed by the harness.
+CONFIGS = {
+    "c1": dict(name="c1", dim=2, ncomp=1, p=2, n=16, noise=0.0, seed=1, init="sinpi",
+               init_seed=101, k=2, rho=0.5, steps=200, cfl_frac=0.5, lshape=False),
+    "c2": dict(name="c2", dim=2, ncomp=1, p=3, n=256, noise=0.2, seed=2, init="modes",
+               init_seed=102, k=2, rho=0.0, steps=500, cfl_frac=0.8, lshape=False),
+    "c3": dict(name="c3", dim=3, ncomp=1, p=2, n=32, noise=0.15, seed=3, init="modes",
+               init_seed=103, k=2, rho=0.0, steps=100, cfl_frac=0.5, lshape=False),
+    "c4": dict(name="c4", dim=3, ncomp=3, p=4, n=96, noise=0.15, seed=4, init="modes",
+               init_seed=104, k=2, rho=0.5, steps=50, cfl_frac=0.5, lshape=False,
+               lam=1.0, mu=1.0, density=1.0),
+    "c5": dict(name="c5", dim=2, ncomp=1, p=3, n=512, noise=0.1, seed=5, init="modes",
+               init_seed=105, k=2, rho=0.3, steps=200, cfl_frac=0.5, lshape=True),
+}
+
+
+def config(name: str, **over) -> dict:
+    c = dict(CONFIGS[name])
+    c.update(over)
+    return c
+
+
+def make_problem(cfg: dict):
+    """Patches and per-patch initial displacement at every control point.
+
+    Returns dict(patches=[(cell, ctrl)], u0=[per-patch array (m^dim, ncomp)]).
+    Values at Dirichlet control points are returned too; consumers drop them."""
+    dim, p, n = cfg["dim"], cfg["p"], cfg["n"]
+    if cfg.get("lshape"):
+        patches = lshape_patches(p, n, cfg["noise"], cfg["seed"])
+    else:
+        patches = [((0,) * dim, control_net(dim, p, n, cfg["noise"], cfg["seed"]))]
+    ncomp = cfg.get("ncomp", 1)
+    u0 = []
+    if cfg["init"] == "sinpi":
+        for _, ctrl in patches:
+            u0.append(np.stack([sinpi_product(ctrl)] * ncomp, axis=1))
+    else:
+        amps = [sine_modes(cfg["init_seed"] + 1000 * c) for c in range(ncomp)]
+        for _, ctrl in patches:
+            u0.append(np.stack([eval_modes(a, ctrl) for a in amps], axis=1))
+    return dict(patches=patches, u0=u0)

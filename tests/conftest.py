@@ -1,0 +1,23 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu)")
+    config.addinivalue_line("markers", "slow: long CPU oracle run")
+
+
+def pytest_collection_modifyitems(config, items):
+    # a test that imports torch.cuda paths must carry the gpu marker; nothing to do here
+    pass
+
+
+@pytest.fixture(scope="session")
+def root():
+    return ROOT

@@ -1,0 +1,166 @@
+"""Pins for oracle/integrator.py: temporal order 2k,
+exact modal decomposition through the amplification matrix, spatial order
+p+1 against the closed-form wave solution (BASELINE.json configs[0]),
+dissipation / stability behaviour."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import synth
+from oracle import assembly, integrator, params, spectral
+
+
+def _orders(errs):
+    e = np.asarray(errs)
+    return np.log2(e[:-1] / e[1:])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("rho", [0.0, 0.5, 1.0])
+def test_scalar_ode_order_2k(k, rho):
+    # u'' = -w^2 u, u(0)=1, v(0)=0: exact u = cos(w t), v = -w sin(w t)
+    w, T = 1.0, 4.0
+    K = np.array([[w * w]])
+    errs_u, errs_v = [], []
+    taus = [0.2 / 2 ** i for i in range(5)] if k < 3 else [0.4 / 2 ** i for i in range(4)]
+    for tau in taus:
+        it = integrator.Integrator(np.eye(1), K, k, rho, tau, solver=lambda b: b)
+        c = it.init(np.array([1.0]), np.array([0.0]))
+        eu = ev = 0.0  # max error over the trajectory (robust to sign changes)
+        for n in range(1, int(round(T / tau)) + 1):
+            c = it.step(c)
+            eu = max(eu, abs(c[0][0] - math.cos(w * n * tau)))
+            ev = max(ev, abs(c[1][0] + w * math.sin(w * n * tau)))
+        errs_u.append(eu)
+        errs_v.append(ev)
+    ou, ov = _orders(errs_u), _orders(errs_v)
+    assert ou[-1] > 2 * k - 0.35, (ou, errs_u)
+    assert ov[-1] > 2 * k - 0.35, (ov, errs_v)
+
+
+@pytest.fixture(scope="module")
+def c1_disc():
+    cfg = synth.config("c1")
+    prob = synth.make_problem(cfg)
+    d = assembly.Discretization(prob["patches"], cfg["p"], cfg["n"], cfg["dim"])
+    ev, Phi = sla.eigh(d.K.toarray(), d.M.toarray())
+    return cfg, prob, d, ev, Phi
+
+
+def _mnorm(M, x):
+    return math.sqrt(x @ (M @ x))
+
+
+def test_c1_lambda_max_and_cfl(c1_disc):
+    cfg, prob, d, ev, Phi = c1_disc
+    # identity map p=2: lambda_max h^2 = d * 10, i.e. 5120 for h = 1/16
+    assert abs(ev[-1] - 5120.0) < 1e-8 * 5120
+    dt = 0.5 * math.sqrt(params.theta_max_closed_form(0.5) / ev[-1])
+    assert abs(dt - 0.0130427) < 1e-6
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_c1_temporal_order_vs_semidiscrete_exact(c1_disc, k):
+    # BASELINE.json configs[0]: dt = 0.5 CFL, 200 steps, then dt/2, /4, /8
+    cfg, prob, d, ev, Phi = c1_disc
+    M = d.M
+    u0 = d.restrict_local([u[:, 0] for u in prob["u0"]])
+    dt0 = 0.5 * math.sqrt(params.theta_max_closed_form(0.5) / ev[-1])
+    T = 200 * dt0
+    # U(t) = Phi cos(sqrt(Lambda) t) Phi^T M U0 (Phi M-orthonormal)
+    coef = Phi.T @ (M @ u0)
+    U_ex = Phi @ (np.cos(np.sqrt(ev) * T) * coef)
+    V_ex = Phi @ (-np.sqrt(ev) * np.sin(np.sqrt(ev) * T) * coef)
+    eu, evv = [], []
+    for lvl in range(4):
+        dt = dt0 / 2 ** lvl
+        it = integrator.Integrator(M, d.K, k, 0.5, dt)
+        c = it.run(u0, np.zeros_like(u0), 200 * 2 ** lvl)
+        eu.append(_mnorm(M, c[0] - U_ex) / _mnorm(M, U_ex))
+        evv.append(_mnorm(M, c[1] - V_ex) / _mnorm(M, V_ex))
+    ou = _orders(eu)
+    assert np.all(ou > 2 * k - 0.2), (ou, eu)
+    assert _orders(evv)[-1] > 2 * k - 0.3
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("rho", [0.5, 1.0])
+def test_c1_modal_exactness(c1_disc, k, rho):
+    # n steps of the stepper equal the modal map sum_i phi_i G(tau^2 lambda_i)^n
+    cfg, prob, d, ev, Phi = c1_disc
+    M = d.M
+    u0 = d.restrict_local([u[:, 0] for u in prob["u0"]])
+    v0 = 0.3 * u0
+    dt = 0.5 * math.sqrt(params.theta_max_closed_form(rho) / ev[-1])
+    it = integrator.Integrator(M, d.K, k, rho, dt)
+    chain = it.init(u0, v0)
+    nst = 60
+    c = it.run(None, None, nst, chain=chain)
+    Md = M.toarray()
+    # modal coordinates of the chain, scaled as [U, tau V, tau^2 A, ...]
+    Z = np.stack([dt ** m * (Phi.T @ (Md @ chain[m])) for m in range(3 * k)])  # (3k, N)
+    out = np.zeros_like(Z)
+    for i in range(len(ev)):
+        G = spectral.amplification(dt * dt * ev[i], k, rho)
+        out[:, i] = np.linalg.matrix_power(G, nst) @ Z[:, i]
+    for m in range(3):
+        ref = Phi @ (out[m] / dt ** m)
+        assert _mnorm(M, c[m] - ref) / _mnorm(M, ref) < 1e-10, m
+
+
+def test_c1_spatial_convergence_closed_form():
+    # exact u = cos(sqrt(2) pi t) sin(pi x) sin(pi y) (BASELINE.json configs[0]);
+    # L2 projection of u0; error O(h^{p+1}) in L2
+    errs = {}
+    for p in (2, 3):
+        for n in (4, 8, 16):
+            ctrl = synth.control_net(2, p, n)
+            d = assembly.Discretization([((0, 0), ctrl)], p, n, 2)
+            Q = assembly.PatchQuad(ctrl, p, n, 2)
+            free = assembly.interior_mask(n + p, 2)
+            Bf = Q.B[:, free]
+            xq = Q.B @ ctrl
+            W = Q.w * Q.detJ
+            u0q = np.sin(np.pi * xq[:, 0]) * np.sin(np.pi * xq[:, 1])
+            U0 = integrator.DirectMassSolver(d.M)(Bf.T @ (W * u0q))
+            T, dt = 0.5, 2.5e-3 / (n / 4)
+            it = integrator.Integrator(d.M, d.K, 2, 0.5, dt)
+            c = it.run(U0, np.zeros_like(U0), int(round(T / dt)))
+            ex = math.cos(math.sqrt(2) * math.pi * T) * u0q
+            e = Bf @ c[0] - ex
+            errs[(p, n)] = math.sqrt((W * e * e).sum() / (W * ex * ex).sum())
+    for p in (2, 3):
+        r = _orders([errs[(p, n)] for n in (4, 8, 16)])
+        assert r[-1] > p + 1 - 0.3, (p, r)
+    assert 3e-5 < errs[(2, 16)] < 8e-5  # ~5.2e-5
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_c1_energy_and_top_mode_dissipation(c1_disc, k):
+    # Reading R4: the physical energy is not monotone, but on
+    # smooth data its drift is bounded and the highest mode is damped (rho<1)
+    cfg, prob, d, ev, Phi = c1_disc
+    M, K = d.M, d.K
+    dt = 0.5 * math.sqrt(params.theta_max_closed_form(0.5) / ev[-1])
+    E = lambda c: 0.5 * (c[1] @ (M @ c[1]) + c[0] @ (K @ c[0]))
+    u0 = d.restrict_local([u[:, 0] for u in prob["u0"]])
+    it = integrator.Integrator(M, K, k, 0.5, dt)
+    c = it.run(u0, np.zeros_like(u0), 200)
+    E0 = E(it.init(u0, np.zeros_like(u0)))
+    assert abs(E(c) / E0 - 1) < (5e-3 if k == 1 else 1e-5)
+    top = Phi[:, -1]
+    c = it.run(top, np.zeros_like(top), 200)
+    assert E(c) / E(it.init(top, np.zeros_like(top))) < (0.01 if k == 1 else 0.95)
+
+
+def test_c1_instability_above_cfl(c1_disc):
+    # beyond Theta_max the top mode grows without bound (CFL condition)
+    cfg, prob, d, ev, Phi = c1_disc
+    top = Phi[:, -1]
+    for fac, grows in ((0.97, False), (1.03, True)):
+        dt = fac * math.sqrt(params.theta_max_closed_form(0.5) / ev[-1])
+        it = integrator.Integrator(d.M, d.K, 2, 0.5, dt)
+        c = it.run(top, np.zeros_like(top), 400)
+        assert (np.abs(c[0]).max() > 1e3) == grows
