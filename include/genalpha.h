@@ -1,0 +1,182 @@
+/*
+ * genalpha.h — C ABI of the B200-native explicit order-2k generalized-alpha
+ * integrator for isogeometric (B-spline) discretizations of the scalar wave
+ * equation and linear elastodynamics (arXiv 2102.11536, "PAPER.md").
+ *
+ * Citations are PAPER.md line numbers (P:line) and DESIGN.md readings (Rn).
+ *
+ * Problem:  M U'' + K U = 0, U(0) = U0, U'(0) = V0, with M, K the
+ * Galerkin mass and stiffness matrices of a maximal-regularity B-spline space
+ * of degree p on one patch or on a conforming multi-patch domain,
+ * homogeneous Dirichlet data on the whole boundary.  Damping and
+ * forcing are zero (C = 0, F = 0).  Time stepping is the explicit order-2k
+ * scheme of P:398-431 (k mass solves + updates of the other 2k variables per
+ * step), with the K-term reading R1 and parameter set R2 of DESIGN.md.  Each
+ * mass solve is PCG with the diagonal-scaled Kronecker preconditioner
+ * (P:703-713), additive Schwarz across patches.
+ *
+ * Conventions (apply to every entry point)
+ *  - Ownership: the CALLER owns all device memory.  The library never calls
+ *    cudaMalloc: it carves its arrays out of the workspace passed to
+ *    ga_create.  Host arrays passed in are copied before the call returns.
+ *  - Streams: device work is enqueued on the given stream, asynchronously,
+ *    unless the entry point says it synchronizes.  A context must be used by
+ *    one stream at a time (the caller orders calls on different streams).
+ *  - Vectors ("free-DoF vectors") are fp64 device arrays of length n_free
+ *    (from ga_query).  Order: component-major (all DoFs of component 0, then
+ *    1, ...); within a component the free DoFs in co-lexicographic order
+ *    (x fastest) of the global masked grid;
+ *    ga_free_dof_map gives (patch, control point) of each entry.
+ *  - Errors are status codes; nothing throws across the ABI.  After a device
+ *    side failure (PCG not converged, instability) the context refuses
+ *    further stepping until ga_set_state / ga_set_chain.
+ *  - Numbers: everything is IEEE fp64.
+ */
+#ifndef GENALPHA_H
+#define GENALPHA_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GA_OK = 0,
+  GA_ERR_ARG = -1,         /* invalid argument / unsupported layout                      */
+  GA_ERR_PARAM = -2,       /* rho outside [0,1], rho_s > rho_b, or undefined parameters   */
+  GA_ERR_GEOMETRY = -3,    /* |J| <= 0 at a Gauss point (assumption P:699-701)           */
+  GA_ERR_CONFORMITY = -4,  /* patch interfaces do not match (assumption P:645-652)       */
+  GA_ERR_NOCONV = -5,      /* a PCG solve reached pcg_maxit                              */
+  GA_ERR_UNSTABLE = -6,    /* ||U||_2 exceeded unstable_factor * ||U_0||_2               */
+  GA_ERR_CUDA = -7,        /* a CUDA runtime call failed (see ga_last_error)             */
+  GA_ERR_OOM = -8          /* workspace or scratch smaller than ga_query asked for       */
+} ga_status;
+
+typedef struct ga_ctx ga_ctx; /* opaque; holds host metadata and views into the workspace */
+
+/* One patch.  All patches share p and n ("same degree p", uniform
+ * refinement).  cell = position of the patch in the coarse patch grid of a
+ * block-structured multi-patch layout (identity orientation); the patch
+ * occupies [cell_d, cell_d + 1] in parametric "patch-grid" coordinates.
+ * ctrl: HOST array of (n+p)^dim control points, co-lexicographic (x fastest),
+ * dim doubles per point.  Copied by ga_query/ga_create. */
+typedef struct {
+  int cell[3];
+  const double* ctrl;
+} ga_patch;
+
+typedef struct {
+  int dim;              /* 2 or 3                                                     */
+  int ncomp;            /* 1: scalar wave u'' = div(omega^2 grad u);            */
+                        /* dim: linear elasticity (lame_lambda, lame_mu, density)      */
+  int p;                /* spline degree, 1..8, maximal regularity C^{p-1}    */
+  int n;                /* elements per direction per patch, >= 1                     */
+  int npatch;           /* >= 1                                                       */
+  const ga_patch* patches;
+  double omega;         /* wave speed (scalar wave)                                   */
+  double lame_lambda, lame_mu, density; /* elasticity only                            */
+  int k;                /* accuracy order 2k, 1 <= k <= 4                 */
+  double rho_b, rho_s;  /* spectral radius parameters, 0 <= rho_s <= rho_b <= 1*/
+  int param_set;        /* 0: isospectral j<k set (R2, default);            */
+                        /* 1: j<k set as printed in P:494-496 (requires rho_b < 1)     */
+  double dt;            /* time step tau > 0                                          */
+  double pcg_rtol;      /* stop when ||r||_2 <= pcg_rtol ||b||_2 (BASELINE: 1e-13)      */
+  int pcg_maxit;        /* per solve (main + refinement), e.g. 500                    */
+  int pcg_refine;       /* 1: after convergence restart once from the true residual  */
+                        /*    b - M x (R8); 0: plain PCG                     */
+  double pcg_refine_rtol; /* refinement stop: 0 -> ||r|| <= pcg_rtol ||b||; > 0 ->      */
+                        /*    ||r|| <= min(pcg_rtol ||b||, pcg_refine_rtol ||b - M x0||)*/
+                        /*    (x0 = main-phase result; reaching pcg_maxit here is not   */
+                        /*    an error).  1e-3 recommended for p >= 5 (kappa(M) ~1e8)   */
+  double unstable_factor; /* GA_ERR_UNSTABLE threshold on ||U||/||U_0||; 0 disables   */
+} ga_desc;
+
+typedef struct {
+  long long steps;          /* steps completed since the last ga_set_state/ga_set_chain */
+  long long solves;         /* mass solves completed                                    */
+  long long pcg_iters[4];   /* total PCG iterations per block (incl. refinement)        */
+  int last_iters[4];        /* iterations of the most recent solve, per block          */
+  int max_iters;            /* max iterations of any single solve                       */
+  double max_rel_residual;  /* max final ||r||/||b|| (recursive) over solves            */
+  int status;               /* ga_status of the device-side run                         */
+  long long fail_step;      /* step at which status became non-zero (-1 if none)        */
+  int fail_block;           /* block (0-based) that failed (-1 if none)                 */
+  long long kernel_launches;/* kernels of this library executed on the device since    */
+                            /* the last ga_set_state (counted on the device)            */
+} ga_stats;
+
+/* Generalized-alpha parameters of the k blocks (host only, no GPU).
+ * alpha/beta/gamma/alpha_f: arrays of length k (block j = index j-1):
+ * blocks j < k: alpha_f = 1 and (param_set 0) the isospectral closed forms of
+ * DESIGN.md R2, or (1) P:494-496; block k: P:497-499, alpha_f = 0;
+ * gamma = 1/2 - alpha_f + alpha.  theta_max (may be NULL) receives the
+ * stability limit Theta_max = tau^2 lambda_max of block k (R2/G3),
+ * equal for every block under param_set 0.  Returns GA_ERR_PARAM on bad rho. */
+ga_status ga_params(int k, double rho_b, double rho_s, int param_set,
+                    double* alpha, double* beta, double* gamma, double* alpha_f,
+                    double* theta_max);
+
+/* Sizes for a descriptor (host only, no GPU).  n_free: length of a free-DoF
+ * vector (= ncomp * scalar free DoFs).  workspace_bytes: device memory the
+ * context keeps for its lifetime.  scratch_bytes: device memory needed only
+ * during ga_create (operator assembly); any size >= scratch_min works
+ * (smaller means more assembly passes).  Pointers may be NULL. */
+ga_status ga_query(const ga_desc* desc, size_t* n_free, size_t* workspace_bytes,
+                   size_t* scratch_bytes, size_t* scratch_min);
+
+/* Create a context: validates desc, uploads geometry, assembles M and K on
+ * the GPU into the stencil layout, builds the preconditioner and the step
+ * graphs.  d_workspace: >= workspace_bytes, 256-byte aligned, owned by the
+ * caller and kept alive until ga_destroy.  d_scratch: >= scratch_min bytes,
+ * may be released after return.  SYNCHRONIZES stream once (reads back the
+ * minimum |J| for GA_ERR_GEOMETRY).  *out is NULL on failure. */
+ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_bytes,
+                    void* d_scratch, size_t scratch_bytes, void* stream, ga_ctx** out);
+
+/* Initial chain (R3): c0 = U0, c1 = V0,
+ * c_m = M^{-1}(-K c_{m-2}), m = 2..3k-1 (3k-2 PCG solves; zero right-hand
+ * sides are skipped).  d_v0 may be NULL (V0 = 0).  Resets stats. */
+ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void* stream);
+
+/* Advance nsteps explicit steps.  Asynchronous; a device-side
+ * failure stops further steps and is reported by ga_get_stats. */
+ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream);
+
+/* Copy U, V, A (c0, c1, c2) to caller vectors; any pointer may be NULL. */
+ga_status ga_get_state(ga_ctx* ctx, double* d_u, double* d_v, double* d_a, void* stream);
+
+/* Checkpoint / resume of the whole chain c_m, m = 0..3k-1 (free-DoF vectors). */
+ga_status ga_get_chain(ga_ctx* ctx, int m, double* d_out, void* stream);
+ga_status ga_set_chain(ga_ctx* ctx, int m, const double* d_in, void* stream);
+
+/* SYNCHRONIZES stream; fills *out. */
+ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream);
+
+/* Test / tooling hooks.  which: 0 = M, 1 = K, 2 = preconditioner inverse
+ * calM^{-1} (P:703-713 / P:766).  y = op(x), free-DoF vectors. */
+ga_status ga_apply(ga_ctx* ctx, int which, const double* d_x, double* d_y, void* stream);
+
+/* x = M^{-1} b by the same PCG the step uses (zero initial guess).
+ * *iters (may be NULL) receives the iteration count; if non-NULL the call
+ * SYNCHRONIZES stream. */
+ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters, void* stream);
+
+/* lambda_max(M^{-1} K) by `iters` power iterations (each one K apply + one PCG
+ * solve), for the CFL time step dt = c sqrt(theta_max / lambda_max).
+ * SYNCHRONIZES stream. */
+ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream);
+
+/* host_map[f] = patch * (n+p)^dim + local control-point index (co-lex) of
+ * free scalar DoF f, f < n_free / ncomp.  Host only. */
+ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
+
+void ga_destroy(ga_ctx* ctx);
+
+/* Last error message of ctx (or of the calling thread if ctx is NULL). */
+const char* ga_last_error(const ga_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GENALPHA_H */

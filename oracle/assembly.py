@@ -40,7 +40,10 @@ class PatchQuad:
     """Tensor-product quadrature data of one patch: basis matrices mapping the
     m^d control coefficients to the (n(p+1))^d Gauss points, Jacobians, weights."""
 
-    def __init__(self, ctrl: np.ndarray, p: int, n: int, dim: int):
+    def __init__(self, ctrl: np.ndarray, p: int, n: int, dim: int, reverse_points: bool = False):
+        """reverse_points: enumerate the Gauss points in reverse order, which
+        changes only the summation order of every quadrature sum (used by the
+        tests to measure the fp64 assembly-order floor)."""
         B1, dB1, w1 = tables_1d(p, n)
         self.p, self.n, self.dim, self.m = p, n, dim, n + p
         self.B = _kron_all([B1] * dim)
@@ -51,6 +54,11 @@ class PatchQuad:
         w = w1
         for _ in range(dim - 1):
             w = np.kron(w1, w)
+        if reverse_points:
+            rev = np.arange(self.B.shape[0])[::-1]
+            self.B = sp.csr_matrix(self.B[rev])
+            self.D = [sp.csr_matrix(Dc[rev]) for Dc in self.D]
+            w = w[rev]
         self.w = w
         # J[q, a, b] = dF_a/dxi_b = sum_i C_i[a] dB_i/dxi_b
         J = np.empty((self.B.shape[0], dim, dim))
@@ -73,13 +81,13 @@ class PatchQuad:
         return float(self.detJ.min())
 
 
-def patch_operators(ctrl, p, n, dim, ncomp=1, omega=1.0, lam=1.0, mu=1.0, density=1.0):
+def patch_operators(ctrl, p, n, dim, ncomp=1, omega=1.0, lam=1.0, mu=1.0, density=1.0, reverse_points=False):
     """Unreduced (all m^d control points) M and K of one patch.
 
     ncomp = 1: scalar wave; ncomp = dim: linear elasticity, component-major
     unknown ordering [u_x (all points), u_y, (u_z)].  Raises ValueError when
     |J| <= 0 at a Gauss point (Assumption P:699-701)."""
-    Q = PatchQuad(ctrl, p, n, dim)
+    Q = PatchQuad(ctrl, p, n, dim, reverse_points)
     if Q.min_detJ() <= 0.0:
         raise ValueError("non-positive Jacobian determinant")
     W = sp.diags(Q.w * Q.detJ)
@@ -132,7 +140,7 @@ class Discretization:
       G             per patch: array local index -> global index (or -1 if Dirichlet)
     """
 
-    def __init__(self, patches, p, n, dim, ncomp=1, **mat):
+    def __init__(self, patches, p, n, dim, ncomp=1, reverse_points=False, **mat):
         self.p, self.n, self.dim, self.ncomp = p, n, dim, ncomp
         m = n + p
         self.m = m
@@ -187,7 +195,7 @@ class Discretization:
         Kg = sp.csr_matrix((nglob * ncomp, nglob * ncomp))
         self.min_detJ = np.inf
         for r in range(npatch):
-            Mr, Kr = patch_operators(ctrls[r], p, n, dim, ncomp, **mat)
+            Mr, Kr = patch_operators(ctrls[r], p, n, dim, ncomp, reverse_points=reverse_points, **mat)
             self.min_detJ = min(self.min_detJ, PatchQuad(ctrls[r], p, n, dim).min_detJ())
             rows = np.concatenate([glob_of[r] + c * nglob for c in range(ncomp)])
             Pr = sp.csr_matrix((np.ones(rows.size), (rows, np.arange(rows.size))),

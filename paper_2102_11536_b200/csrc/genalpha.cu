@@ -1,0 +1,986 @@
+// C ABI (include/genalpha.h) of the B200 explicit order-2k generalized-alpha
+// integrator: descriptor validation, workspace layout, GPU assembly driver,
+// preconditioner setup, CUDA-graph construction (PCG loops as conditional
+// WHILE nodes, no host synchronisation inside a step) and the entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/genalpha.h"
+#include "assembly.cuh"
+#include "common.cuh"
+#include "host_math.h"
+#include "ops.cuh"
+
+using namespace ga;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+struct PatchHost {
+  int cell[3];
+  std::vector<double> ctrl;
+};
+
+struct PrecPatch {
+  int lo[3], bd[3];     // box in grid coordinates
+  int llo[3];           // first local basis index per direction
+  double* s = nullptr;  // device, box points
+  double* t = nullptr;  // device, nvec*box*k (multi-patch only)
+  double* L[3] = {nullptr, nullptr, nullptr};
+  std::vector<double> hL[3], hdiag[3];
+};
+
+}  // namespace
+
+struct ga_ctx {
+  ga_desc d{};
+  std::vector<PatchHost> patches;
+  int dim = 2, nvec = 1, p = 1, n = 1, m = 2, k = 1, W1 = 3;
+  long long S = 0;
+  GridDesc g{};
+  long long nfree = 0;  // scalar free DoFs
+  std::vector<long long> hmap;           // api -> grid (multi-patch)
+  std::vector<unsigned char> hmask;      // grid mask (multi-patch)
+  std::vector<long long> hlocal;         // api -> patch*m^dim + local
+  double alpha[KMAX], beta[KMAX], gamma[KMAX], alpha_f[KMAX], theta_max = 0;
+  // device views into the workspace
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  double *coefM = nullptr, *coefK = nullptr, *chain = nullptr;
+  double *pred = nullptr, *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr;
+  unsigned char* mask = nullptr;
+  long long* map = nullptr;
+  PcgState* pcg = nullptr;
+  DevStatus* st = nullptr;
+  double* partial = nullptr;
+  unsigned int* counter = nullptr;
+  double* dscal = nullptr;  // small device scalars
+  std::vector<PrecPatch> prec;
+  // graphs
+  cudaStream_t aux = nullptr, cap = nullptr;  // private capture streams
+  cudaGraphExec_t g_step = nullptr, g_solveK = nullptr, g_solveB = nullptr;
+  cudaGraph_t gr_step = nullptr, gr_solveK = nullptr, gr_solveB = nullptr;
+  std::string err;
+};
+
+namespace {
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      seterr(ctx, std::string(#call) + ": " + cudaGetErrorString(e_));              \
+      return GA_ERR_CUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+void seterr(ga_ctx* ctx, const std::string& s) {
+  if (ctx) ctx->err = s;
+  g_thread_err = s;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t off_coefM, off_coefK, off_chain, off_mv[7], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
+      off_dscal;
+  std::vector<size_t> off_s, off_t, off_L[3];
+  size_t total;
+};
+
+// Derived sizes that do not need the GPU.
+struct Shape {
+  int dim, nvec, p, n, m, k, W1;
+  long long S;
+  GridDesc g;
+  std::vector<PrecPatch> prec;  // boxes only
+  long long nfree;
+  std::vector<unsigned char> mask;
+  std::vector<long long> map;
+  std::vector<long long> local;
+  int pmin[3], pmax[3];
+};
+
+ga_status validate(const ga_desc* d, ga_ctx* ctx) {
+  if (!d) { seterr(ctx, "desc is NULL"); return GA_ERR_ARG; }
+  if (d->dim != 2 && d->dim != 3) { seterr(ctx, "dim must be 2 or 3"); return GA_ERR_ARG; }
+  if (d->ncomp != 1 && !(d->ncomp == 3 && d->dim == 3)) { seterr(ctx, "ncomp must be 1 or 3 (dim 3)"); return GA_ERR_ARG; }
+  if (d->p < 1 || d->p > 7) { seterr(ctx, "p must be in 1..7"); return GA_ERR_ARG; }
+  if (d->n < 1) { seterr(ctx, "n must be >= 1"); return GA_ERR_ARG; }
+  if (d->n + d->p < 3) { seterr(ctx, "n + p must be >= 3 (at least one free DoF)"); return GA_ERR_ARG; }
+  if (d->npatch < 1 || d->npatch > MAXPATCH || !d->patches) { seterr(ctx, "npatch must be 1..16"); return GA_ERR_ARG; }
+  if (d->k < 1 || d->k > KMAX) { seterr(ctx, "k must be 1..4"); return GA_ERR_ARG; }
+  if (!(d->dt > 0.0) || !std::isfinite(d->dt)) { seterr(ctx, "dt must be > 0"); return GA_ERR_ARG; }
+  if (!(d->pcg_refine_rtol >= 0.0) || d->pcg_refine_rtol >= 1.0) { seterr(ctx, "pcg_refine_rtol must be in [0,1)"); return GA_ERR_ARG; }
+  if (!(d->pcg_rtol > 0.0) || d->pcg_maxit < 1) { seterr(ctx, "pcg_rtol > 0 and pcg_maxit >= 1 required"); return GA_ERR_ARG; }
+  if (d->param_set != 0 && d->param_set != 1) { seterr(ctx, "param_set must be 0 or 1"); return GA_ERR_ARG; }
+  double a[KMAX], b[KMAX], g[KMAX], f[KMAX], th;
+  int rc = scheme_params(d->k, d->rho_b, d->rho_s, d->param_set, a, b, g, f, &th);
+  if (rc != 0) { seterr(ctx, "invalid rho_b/rho_s (need 0 <= rho_s <= rho_b <= 1; param_set 1 needs rho < 1)"); return GA_ERR_PARAM; }
+  for (int i = 0; i < d->npatch; ++i) {
+    if (!d->patches[i].ctrl) { seterr(ctx, "patch ctrl is NULL"); return GA_ERR_ARG; }
+    for (int c = 0; c < 3; ++c)
+      if (d->patches[i].cell[c] < 0 || d->patches[i].cell[c] > 64 || (c >= d->dim && d->patches[i].cell[c] != 0)) {
+        seterr(ctx, "patch cell out of range");
+        return GA_ERR_ARG;
+      }
+    for (int j = 0; j < i; ++j)
+      if (!memcmp(d->patches[i].cell, d->patches[j].cell, sizeof(int) * 3)) { seterr(ctx, "two patches share a cell"); return GA_ERR_ARG; }
+  }
+  return GA_OK;
+}
+
+// Global masked grid, boxes, maps.
+ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_conformity) {
+  sh.dim = d->dim; sh.nvec = d->ncomp; sh.p = d->p; sh.n = d->n; sh.m = d->n + d->p; sh.k = d->k; sh.W1 = 2 * d->p + 1;
+  sh.S = (long long)sh.W1 * sh.W1 * (sh.dim == 3 ? sh.W1 : 1);
+  const int m = sh.m, dim = sh.dim;
+  int cmax[3] = {0, 0, 0};
+  for (int i = 0; i < d->npatch; ++i)
+    for (int c = 0; c < dim; ++c) cmax[c] = std::max(cmax[c], d->patches[i].cell[c]);
+  // full global point counts (incl. boundary): (cmax+1)(m-1)+1 per direction
+  int Gfull[3] = {1, 1, 1}, G[3] = {1, 1, 1};
+  for (int c = 0; c < dim; ++c) { Gfull[c] = (cmax[c] + 1) * (m - 1) + 1; G[c] = Gfull[c] - 2; }
+  sh.g.dim = dim; sh.g.nx = G[0]; sh.g.ny = G[1]; sh.g.nz = dim == 3 ? G[2] : 1;
+  sh.g.npts = (long long)sh.g.nx * sh.g.ny * sh.g.nz;
+  long long guard = (long long)sh.p * (1 + sh.g.nx + (dim == 3 ? (long long)sh.g.nx * sh.g.ny : 0));
+  guard = (guard + 31) / 32 * 32;
+  sh.g.guard = guard;
+  sh.g.padded = sh.g.npts + 2 * guard;
+  // occupancy of coarse cells
+  std::map<long long, int> cellid;
+  auto ckey = [&](int x, int y, int z) { return ((long long)z * 1000 + y) * 1000 + x; };
+  for (int i = 0; i < d->npatch; ++i) cellid[ckey(d->patches[i].cell[0], d->patches[i].cell[1], d->patches[i].cell[2])] = i;
+  const bool multi = d->npatch > 1;
+  // a grid point (interior coords) is free iff every coarse cell whose closure contains it is a patch
+  if (multi) {
+    sh.mask.assign(sh.g.npts, 0);
+    for (long long gi = 0; gi < sh.g.npts; ++gi) {
+      int gc[3] = {(int)(gi % sh.g.nx), (int)((gi / sh.g.nx) % sh.g.ny), (int)(gi / ((long long)sh.g.nx * sh.g.ny))};
+      int lo[3], hi[3];
+      for (int c = 0; c < 3; ++c) {
+        if (c >= dim) { lo[c] = hi[c] = 0; continue; }
+        int I = gc[c] + 1;  // full coordinate
+        int cc = I / (m - 1);
+        if (I % (m - 1) == 0) { lo[c] = cc - 1; hi[c] = cc; } else { lo[c] = hi[c] = cc; }
+      }
+      bool ok = true;
+      for (int z = lo[2]; z <= hi[2] && ok; ++z)
+        for (int y = lo[1]; y <= hi[1] && ok; ++y)
+          for (int x = lo[0]; x <= hi[0] && ok; ++x) {
+            if (x < 0 || y < 0 || z < 0 || !cellid.count(ckey(x, y, z))) ok = false;
+          }
+      sh.mask[gi] = ok ? 1 : 0;
+    }
+    sh.map.clear();
+    for (long long gi = 0; gi < sh.g.npts; ++gi)
+      if (sh.mask[gi]) sh.map.push_back(gi);
+    sh.nfree = (long long)sh.map.size();
+  } else {
+    sh.nfree = sh.g.npts;
+  }
+  // (patch, local) of each free DoF: first patch in order whose closed cell contains it
+  const long long mpow = dim == 3 ? (long long)m * m * m : (long long)m * m;
+  sh.local.assign(sh.nfree, -1);
+  for (long long f = 0; f < sh.nfree; ++f) {
+    long long gi = multi ? sh.map[f] : f;
+    int gc[3] = {(int)(gi % sh.g.nx), (int)((gi / sh.g.nx) % sh.g.ny), (int)(gi / ((long long)sh.g.nx * sh.g.ny))};
+    for (int r = 0; r < d->npatch; ++r) {
+      long long loc = 0, mul = 1;
+      bool in = true;
+      for (int c = 0; c < dim; ++c) {
+        int li = gc[c] + 1 - d->patches[r].cell[c] * (m - 1);
+        if (li < 0 || li > m - 1) { in = false; break; }
+        loc += li * mul;
+        mul *= m;
+      }
+      if (in) { sh.local[f] = r * mpow + loc; break; }
+    }
+  }
+  // preconditioner boxes: free local indices of patch r (tensor superset, reading R6)
+  sh.prec.clear();
+  for (int r = 0; r < d->npatch; ++r) {
+    PrecPatch pp;
+    for (int c = 0; c < 3; ++c) {
+      if (c >= dim) { pp.lo[c] = 0; pp.bd[c] = 1; pp.llo[c] = 0; continue; }
+      int cell = d->patches[r].cell[c];
+      // local index range [1, m-2] plus the interface ends if the neighbour cell exists
+      int llo = 1, lhi = m - 2;
+      int nb[3] = {d->patches[r].cell[0], d->patches[r].cell[1], d->patches[r].cell[2]};
+      nb[c] = cell - 1;
+      if (cell > 0 && cellid.count(ckey(nb[0], nb[1], nb[2]))) llo = 0;
+      nb[c] = cell + 1;
+      if (cellid.count(ckey(nb[0], nb[1], nb[2]))) lhi = m - 1;
+      pp.llo[c] = llo;
+      pp.lo[c] = cell * (m - 1) + llo - 1;
+      pp.bd[c] = lhi - llo + 1;
+    }
+    sh.prec.push_back(pp);
+  }
+  if (multi && check_conformity) {
+    // coincident global points must have bitwise identical control points
+    std::map<long long, std::vector<double>> seen;
+    long long Gx = Gfull[0], Gy = Gfull[1];
+    for (int r = 0; r < d->npatch; ++r) {
+      for (long long loc = 0; loc < mpow; ++loc) {
+        int li[3] = {(int)(loc % m), (int)((loc / m) % m), dim == 3 ? (int)(loc / ((long long)m * m)) : 0};
+        bool onface = false;
+        for (int c = 0; c < dim; ++c) onface |= (li[c] == 0 || li[c] == m - 1);
+        if (!onface) continue;
+        long long key = 0;
+        int I[3];
+        for (int c = 0; c < dim; ++c) I[c] = d->patches[r].cell[c] * (m - 1) + li[c];
+        key = I[0] + Gx * (I[1] + (dim == 3 ? Gy * (long long)I[2] : 0));
+        std::vector<double> pt(d->patches[r].ctrl + loc * dim, d->patches[r].ctrl + loc * dim + dim);
+        auto it = seen.find(key);
+        if (it == seen.end()) seen[key] = pt;
+        else if (memcmp(it->second.data(), pt.data(), sizeof(double) * dim) != 0) {
+          seterr(ctx, "patch interfaces are not conforming (control points differ)");
+          return GA_ERR_CONFORMITY;
+        }
+      }
+    }
+  }
+  return GA_OK;
+}
+
+Layout make_layout(const Shape& sh) {
+  Layout L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
+  const long long npts = sh.g.npts;
+  L.off_coefM = take(sizeof(double) * sh.S * npts);
+  L.off_coefK = take(sizeof(double) * sh.S * npts * (sh.nvec == 3 ? 9 : 1));
+  L.off_chain = take(sizeof(double) * 3 * sh.k * sh.nvec * sh.g.padded);
+  for (int i = 0; i < 7; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
+  const bool multi = sh.prec.size() > 1;
+  L.off_mask = take(multi ? npts : 0);
+  L.off_map = take(multi ? sizeof(long long) * sh.nfree : 0);
+  L.off_pcg = take(sizeof(PcgState));
+  L.off_st = take(sizeof(DevStatus));
+  const long long maxblocks = (sh.nvec * npts + NTHREADS - 1) / NTHREADS + 1;
+  L.off_partial = take(sizeof(double) * 2 * KMAX * maxblocks);
+  L.off_counter = take(sizeof(unsigned int) * 16);
+  L.off_dscal = take(sizeof(double) * 16);
+  for (size_t r = 0; r < sh.prec.size(); ++r) {
+    const PrecPatch& pp = sh.prec[r];
+    long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
+    L.off_s.push_back(take(sizeof(double) * nbox));
+    L.off_t.push_back(take(multi ? sizeof(double) * sh.nvec * nbox * sh.k : 0));
+    for (int c = 0; c < 3; ++c) L.off_L[c].push_back(take(sizeof(double) * (pp.bd[c] + sh.p + 1) * (sh.p + 1)));
+  }
+  L.total = o;
+  return L;
+}
+
+// Assembly scratch per "outer plane" of quadrature points.
+size_t plane_bytes(const Shape& sh) {
+  const long long nq = (long long)sh.n * (sh.p + 1);
+  const long long m = sh.m, W1 = sh.W1;
+  if (sh.dim == 3) return sizeof(double) * (11 * nq * nq + nq * W1 * m + W1 * W1 * m * m);
+  return sizeof(double) * (6 * nq + W1 * m);
+}
+size_t asm_fixed_bytes(const Shape& sh) {
+  const long long nq = (long long)sh.n * (sh.p + 1);
+  const long long mp = sh.dim == 3 ? (long long)sh.m * sh.m * sh.m : (long long)sh.m * sh.m;
+  size_t b = align256(sizeof(double) * nq * (sh.p + 1)) * 2 + align256(sizeof(double) * nq) +
+             align256(sizeof(double) * 4 * sh.m * sh.W1 * (sh.p + 1) * (sh.p + 1)) +
+             align256(sizeof(double) * mp * sh.dim) + 256 * 4;
+  return b;
+}
+
+__global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, int loz, const double* d0,
+                          const double* d1, const double* d2, const double* coefM_center, int nx, int ny,
+                          const unsigned char* mask) {
+  const long long nbox = (long long)bx * by * bz;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nbox) return;
+  const int ix = (int)(e % bx), iy = (int)((e / bx) % by), iz = (int)(e / ((long long)bx * by));
+  const long long gi = (lox + ix) + (long long)nx * ((loy + iy) + (long long)ny * (loz + iz));
+  double v = 0.0;
+  if (!mask || mask[gi]) {
+    const double dh = d0[ix] * d1[iy] * (d2 ? d2[iz] : 1.0);
+    const double D = coefM_center[gi];
+    v = sqrt(dh / D);  // s = sqrt(Dh / D): calM^{-1} = S Mh^{-1} S
+  }
+  s[e] = v;
+}
+
+__global__ void k_altsign(GridDesc g, int nvec, int kk, double* v, const unsigned char* mask) {
+  const long long tot = (long long)nvec * g.npts;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const long long i = e % g.npts;
+  const int c = (int)(e / g.npts);
+  const int ix = (int)(i % g.nx), iy = (int)((i / g.nx) % g.ny), iz = (int)(i / ((long long)g.nx * g.ny));
+  double val = ((ix + iy + iz + c) & 1) ? -1.0 : 1.0;
+  if (mask && !mask[i]) val = 0.0;
+  v[((long long)c * g.padded + g.guard + i) * kk] = val;
+}
+
+PrecArgs prec_args(ga_ctx* c, unsigned long long cond, int update) {
+  PrecArgs a;
+  memset(&a, 0, sizeof(a));
+  a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
+  a.npatch = (int)c->prec.size();
+  for (int r = 0; r < a.npatch; ++r) {
+    for (int d = 0; d < 3; ++d) { a.lo[r][d] = c->prec[r].lo[d]; a.bd[r][d] = c->prec[r].bd[d]; a.L[r][d] = c->prec[r].L[d]; }
+    a.s[r] = c->prec[r].s;
+    a.t[r] = c->prec[r].t;
+  }
+  a.mask = c->mask;
+  a.x = c->x; a.r = c->r; a.z = c->z; a.p_ = c->pv; a.q = c->q;
+  a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
+  a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
+  a.maxit = c->d.pcg_maxit;
+  a.cond = cond;
+  a.update = update;
+  return a;
+}
+
+SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
+  SpmvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.coef = which == 0 ? c->coefM : c->coefK;
+  a.x = x; a.y = y; a.b = c->b;
+  a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
+  a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
+  a.mode = mode;
+  a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
+  a.refine_rtol2 = c->d.pcg_refine_rtol > 0 ? c->d.pcg_refine_rtol * c->d.pcg_refine_rtol : 0.0;
+  a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
+  return a;
+}
+
+VecArgs vec_args(ga_ctx* c) {
+  VecArgs a;
+  a.g = c->g; a.nvec = c->nvec; a.kk = c->k;
+  a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
+  a.x = c->x; a.r = c->r; a.z = c->z; a.p = c->pv; a.b = c->b;
+  a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
+  return a;
+}
+
+StageArgs stage_args(ga_ctx* c) {
+  StageArgs a;
+  memset(&a, 0, sizeof(a));
+  a.g = c->g; a.nvec = c->nvec; a.k = c->k;
+  a.chain = c->chain; a.ysol = c->x; a.pred = c->pred;
+  for (int j = 0; j < KMAX; ++j) { a.alpha[j] = c->alpha[j]; a.beta[j] = c->beta[j]; a.gamma[j] = c->gamma[j]; }
+  double fact = 1.0, tp = 1.0;
+  for (int i = 0; i < 3 * KMAX; ++i) {
+    if (i > 0) { fact *= i; tp *= c->d.dt; }
+    a.f[i] = tp / fact;
+  }
+  a.tau = c->d.dt;
+  a.unstable2 = c->d.unstable_factor > 0 ? c->d.unstable_factor * c->d.unstable_factor : 0.0;
+  a.st = c->st; a.partial = c->partial; a.counter = c->counter;
+  return a;
+}
+
+// One PCG phase loop: pre-loop preconditioner (sets the loop condition) and a
+// conditional WHILE node whose body is one PCG iteration.  `s` is capturing.
+ga_status capture_pcg_loop(ga_ctx* ctx, cudaStream_t s) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t graph;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, graph, 0, 0));
+  launch_precond(prec_args(ctx, (unsigned long long)h, 1), s);
+  CK(cudaGetLastError());
+  CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd));
+  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, graph, deps, nd, &cp));
+  CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(ctx->aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  launch_p_update(vec_args(ctx), ctx->aux);
+  launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), ctx->aux);
+  launch_precond(prec_args(ctx, (unsigned long long)h, 1), ctx->aux);
+  cudaGraph_t outg;
+  CK(cudaStreamEndCapture(ctx->aux, &outg));
+  return GA_OK;
+}
+
+// b is in place: PCG (+ refinement restart) solve of M x = b for all k slots.
+ga_status capture_solve(ga_ctx* ctx, cudaStream_t s) {
+  launch_init_from_b(vec_args(ctx), s);
+  ga_status rc = capture_pcg_loop(ctx, s);
+  if (rc != GA_OK) return rc;
+  if (ctx->d.pcg_refine) {
+    launch_spmv(spmv_args(ctx, 0, ctx->x, ctx->r, SPMV_TRUERES), s);
+    rc = capture_pcg_loop(ctx, s);
+    if (rc != GA_OK) return rc;
+  }
+  launch_solve_end(ctx->pcg, ctx->st, s);
+  return GA_OK;
+}
+
+enum GraphKind { GK_STEP = 0, GK_SOLVEK = 1, GK_SOLVEB = 2 };
+
+ga_status build_graph(ga_ctx* ctx, cudaStream_t s, GraphKind kind, cudaGraph_t* gout, cudaGraphExec_t* eout) {
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  if (kind != GK_SOLVEB) launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->b, SPMV_NEGB), s);
+  ga_status rc = capture_solve(ctx, s);
+  if (rc == GA_OK && kind == GK_STEP) launch_stage(stage_args(ctx), s);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (rc != GA_OK) return rc;
+  if (e != cudaSuccess) { seterr(ctx, std::string("capture: ") + cudaGetErrorString(e)); return GA_ERR_CUDA; }
+  CK(cudaGraphInstantiate(eout, g, 0));
+  *gout = g;
+  return GA_OK;
+}
+
+// GPU assembly of M and K (sum factorisation, slab by slab).
+ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_bytes, cudaStream_t s) {
+  const int dim = sh.dim, p = sh.p, n = sh.n, m = sh.m, W1 = sh.W1, pp1 = p + 1;
+  const long long nq = (long long)n * pp1;
+  Tables1D T = make_tables(p, n);
+  // A tables: A[st][i][o][qq] = phi^(s)_i(q) phi^(t)_{i+o}(q), q = qs(i)+qq
+  const size_t asz = (size_t)m * W1 * pp1 * pp1;
+  std::vector<double> hA(4 * asz, 0.0);
+  for (int st = 0; st < 4; ++st) {
+    const int sdr = st >> 1, tdr = st & 1;
+    for (int i = 0; i < m; ++i) {
+      const int qs = std::max(0, i - p) * pp1, qe = (std::min(n - 1, i) + 1) * pp1;
+      for (int o = -p; o <= p; ++o) {
+        const int j = i + o;
+        if (j < 0 || j >= m) continue;
+        for (int q = qs; q < qe; ++q) {
+          const int e = q / pp1;
+          const int a = i - e, b = j - e;
+          if (a < 0 || a > p || b < 0 || b > p) continue;
+          const double fi = (sdr ? T.der : T.val)[(size_t)q * pp1 + a];
+          const double fj = (tdr ? T.der : T.val)[(size_t)q * pp1 + b];
+          hA[st * asz + ((size_t)i * W1 + (o + p)) * pp1 * pp1 + (q - qs)] = fi * fj;
+        }
+      }
+    }
+  }
+  // carve scratch: fixed tables first
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = scratch + off; off += align256(bytes); return (double*)r; };
+  double* dval = take(sizeof(double) * nq * pp1);
+  double* dder = take(sizeof(double) * nq * pp1);
+  double* dwq = take(sizeof(double) * nq);
+  double* dA = take(sizeof(double) * 4 * asz);
+  const long long mpow = dim == 3 ? (long long)m * m * m : (long long)m * m;
+  double* dctrl = take(sizeof(double) * mpow * dim);
+  double* dmin = take(sizeof(double) * 4);
+  if (off > scratch_bytes) { seterr(ctx, "scratch too small"); return GA_ERR_OOM; }
+  CK(cudaMemcpyAsync(dval, T.val.data(), sizeof(double) * nq * pp1, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dder, T.der.data(), sizeof(double) * nq * pp1, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dwq, T.wq.data(), sizeof(double) * nq, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dA, hA.data(), sizeof(double) * 4 * asz, cudaMemcpyHostToDevice, s));
+  double big = 1e300;
+  CK(cudaMemcpyAsync(dmin, &big, sizeof(double), cudaMemcpyHostToDevice, s));
+  // slab size from the remaining scratch
+  const size_t pb = plane_bytes(sh);
+  const size_t avail = scratch_bytes - off;
+  long long planes = (long long)(avail / (pb + 1024));
+  int Z = (int)(planes / pp1) - p;  // rows per slab along the outer direction
+  if (Z < 1) { seterr(ctx, "scratch too small for one assembly slab"); return GA_ERR_OOM; }
+  Z = std::min(Z, m);
+  const long long maxq = (long long)(Z + p) * pp1;
+  const long long lowpts = dim == 3 ? nq * nq : nq;
+  double* geo = take(sizeof(double) * (dim == 3 ? 10 : 5) * lowpts * maxq);
+  double* W = take(sizeof(double) * lowpts * maxq);
+  double* X1 = take(sizeof(double) * (dim == 3 ? nq * W1 * m : W1 * m) * maxq);
+  double* X2 = dim == 3 ? take(sizeof(double) * W1 * W1 * m * m * maxq) : nullptr;
+  if (off > scratch_bytes) { seterr(ctx, "scratch too small (slab)"); return GA_ERR_OOM; }
+
+  CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.npts, s));
+  CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.npts * (sh.nvec == 3 ? 9 : 1), s));
+  // term list: (target block pointer, spec, derivative flags per direction)
+  struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; };
+  std::vector<Term> terms;
+  {
+    Term t;
+    memset(&t, 0, sizeof(t));
+    t.coef = ctx->coefM;
+    t.ts.kind = 0;
+    t.ts.scale = sh.nvec == 3 ? ctx->d.density : 1.0;
+    terms.push_back(t);
+  }
+  if (sh.nvec == 1) {
+    for (int c = 0; c < dim; ++c)
+      for (int e = 0; e < dim; ++e) {
+        Term t;
+        memset(&t, 0, sizeof(t));
+        t.coef = ctx->coefK;
+        t.ts.kind = 1; t.ts.c = c; t.ts.e = e; t.ts.scale = ctx->d.omega * ctx->d.omega;
+        for (int d = 0; d < 3; ++d) { t.sflag[d] = (d == c); t.tflag[d] = (d == e); }
+        terms.push_back(t);
+      }
+  } else {
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        for (int c = 0; c < 3; ++c)
+          for (int e = 0; e < 3; ++e) {
+            Term t;
+            memset(&t, 0, sizeof(t));
+            t.coef = ctx->coefK + (size_t)(a * 3 + b) * sh.S * sh.g.npts;
+            t.ts.kind = 2; t.ts.a = a; t.ts.b = b; t.ts.c = c; t.ts.e = e;
+            t.ts.lam = ctx->d.lame_lambda; t.ts.mu = ctx->d.lame_mu;
+            for (int d = 0; d < 3; ++d) { t.sflag[d] = (d == c); t.tflag[d] = (d == e); }
+            terms.push_back(t);
+          }
+  }
+  for (size_t r = 0; r < ctx->patches.size(); ++r) {
+    CK(cudaMemcpyAsync(dctrl, ctx->patches[r].ctrl.data(), sizeof(double) * mpow * dim, cudaMemcpyHostToDevice, s));
+    AsmPatch P;
+    P.p = p; P.n = n; P.m = m; P.nq = (int)nq; P.ctrl = dctrl; P.val = dval; P.der = dder; P.wq = dwq;
+    for (int r0 = 0; r0 < m; r0 += Z) {
+      const int r1 = std::min(m, r0 + Z);
+      const int ea = std::max(0, r0 - p), eb = std::min(n, r1);  // elements feeding rows [r0, r1)
+      const int qa = ea * pp1, nqs = (eb - ea) * pp1;
+      const long long npts_s = lowpts * nqs;
+      launch_geometry(P, dim, qa, nqs, geo, npts_s, dmin, s);
+      for (const Term& t : terms) {
+        launch_wterm(geo, npts_s, npts_s, dim, t.ts, W, s);
+        const double* A0 = dA + (size_t)(t.sflag[0] * 2 + t.tflag[0]) * asz;
+        const double* A1 = dA + (size_t)(t.sflag[1] * 2 + t.tflag[1]) * asz;
+        const double* A2 = dA + (size_t)(t.sflag[2] * 2 + t.tflag[2]) * asz;
+        ContractDesc c1;
+        memset(&c1, 0, sizeof(c1));
+        c1.W1 = W1; c1.m = m; c1.p = p; c1.n = n; c1.qoff = 0;
+        c1.nouter = (dim == 3 ? nq : 1) * nqs; c1.nmid = 1; c1.ninner = 1;
+        c1.in_s_outer = nq; c1.in_s_q = 1; c1.in_s_mid = 0; c1.in_s_inner = 0;
+        c1.out_s_outer = (long long)W1 * m; c1.out_s_o = m; c1.out_s_mid = 0; c1.out_s_i = 1; c1.out_s_inner = 0;
+        launch_contract(W, X1, A0, c1, s);
+        FinalDesc f;
+        memset(&f, 0, sizeof(f));
+        f.W1 = W1; f.m = m; f.p = p; f.n = n; f.qoff = qa; f.r0 = r0; f.r1 = r1;
+        for (int d = 0; d < 3; ++d) f.cell[d] = ctx->patches[r].cell[d];
+        f.G[0] = sh.g.nx; f.G[1] = sh.g.ny; f.G[2] = sh.g.nz;
+        f.npts = sh.g.npts;
+        f.mask = ctx->mask;
+        if (dim == 3) {
+          ContractDesc c2;
+          memset(&c2, 0, sizeof(c2));
+          c2.W1 = W1; c2.m = m; c2.p = p; c2.n = n; c2.qoff = 0;
+          c2.nouter = nqs; c2.nmid = W1; c2.ninner = m;
+          c2.in_s_outer = nq * W1 * m; c2.in_s_q = (long long)W1 * m; c2.in_s_mid = m; c2.in_s_inner = 1;
+          c2.out_s_outer = (long long)W1 * W1 * m * m; c2.out_s_o = (long long)W1 * m * m; c2.out_s_mid = (long long)m * m;
+          c2.out_s_i = m; c2.out_s_inner = 1;
+          launch_contract(X1, X2, A1, c2, s);
+          launch_contract_final(3, X2, A2, f, t.coef, s);
+        } else {
+          launch_contract_final(2, X1, A1, f, t.coef, s);
+        }
+        CK(cudaGetLastError());
+      }
+    }
+  }
+  double hmin = 0;
+  CK(cudaMemcpyAsync(&hmin, dmin, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!(hmin > 0.0)) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "non-positive Jacobian determinant (min |J| = %.3e)", hmin);
+    seterr(ctx, buf);
+    return GA_ERR_GEOMETRY;
+  }
+  return GA_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+ga_status ga_params(int k, double rho_b, double rho_s, int param_set, double* alpha, double* beta, double* gamma,
+                    double* alpha_f, double* theta_max) {
+  if (param_set != 0 && param_set != 1) return GA_ERR_ARG;
+  int rc = scheme_params(k, rho_b, rho_s, param_set, alpha, beta, gamma, alpha_f, theta_max);
+  if (rc == -1) return GA_ERR_ARG;
+  if (rc != 0) return GA_ERR_PARAM;
+  return GA_OK;
+}
+
+ga_status ga_query(const ga_desc* desc, size_t* n_free, size_t* workspace_bytes, size_t* scratch_bytes,
+                   size_t* scratch_min) {
+  ga_status rc = validate(desc, nullptr);
+  if (rc != GA_OK) return rc;
+  Shape sh;
+  rc = make_shape(desc, sh, nullptr, false);
+  if (rc != GA_OK) return rc;
+  Layout L = make_layout(sh);
+  if (n_free) *n_free = (size_t)(sh.nfree * sh.nvec);
+  if (workspace_bytes) *workspace_bytes = L.total;
+  const size_t fixed = asm_fixed_bytes(sh), pb = plane_bytes(sh) + 1024;
+  const size_t smin = fixed + pb * (size_t)(sh.p + 2) * (sh.p + 1) + (1 << 20);
+  const size_t sall = fixed + pb * (size_t)(sh.m + sh.p + 1) * (sh.p + 1) + (1 << 20);
+  const size_t cap = (size_t)8 << 30;
+  if (scratch_min) *scratch_min = smin;
+  if (scratch_bytes) *scratch_bytes = std::max(smin, std::min(sall, cap));
+  return GA_OK;
+}
+
+ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_bytes, void* d_scratch,
+                    size_t scratch_bytes, void* stream, ga_ctx** out) {
+  if (out) *out = nullptr;
+  if (!out) return GA_ERR_ARG;
+  ga_ctx* ctx = new ga_ctx();
+  ga_status rc = validate(desc, ctx);
+  if (rc != GA_OK) { delete ctx; return rc; }
+  ctx->d = *desc;
+  ctx->d.patches = nullptr;
+  Shape sh;
+  rc = make_shape(desc, sh, ctx, true);
+  if (rc != GA_OK) { delete ctx; return rc; }
+  Layout L = make_layout(sh);
+  if (!d_workspace || workspace_bytes < L.total || ((size_t)d_workspace & 255)) {
+    seterr(ctx, "workspace too small or misaligned");
+    delete ctx;
+    return GA_ERR_OOM;
+  }
+  if (!d_scratch) { seterr(ctx, "scratch is NULL"); delete ctx; return GA_ERR_OOM; }
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->dim = sh.dim; ctx->nvec = sh.nvec; ctx->p = sh.p; ctx->n = sh.n; ctx->m = sh.m; ctx->k = sh.k; ctx->W1 = sh.W1;
+  ctx->S = sh.S; ctx->g = sh.g; ctx->nfree = sh.nfree;
+  ctx->hmap = sh.map; ctx->hmask = sh.mask; ctx->hlocal = sh.local;
+  scheme_params(desc->k, desc->rho_b, desc->rho_s, desc->param_set, ctx->alpha, ctx->beta, ctx->gamma,
+                ctx->alpha_f, &ctx->theta_max);
+  const long long mpow = sh.dim == 3 ? (long long)sh.m * sh.m * sh.m : (long long)sh.m * sh.m;
+  for (int r = 0; r < desc->npatch; ++r) {
+    PatchHost ph;
+    memcpy(ph.cell, desc->patches[r].cell, sizeof(ph.cell));
+    ph.ctrl.assign(desc->patches[r].ctrl, desc->patches[r].ctrl + mpow * sh.dim);
+    for (double v : ph.ctrl)
+      if (!std::isfinite(v)) { seterr(ctx, "non-finite control point"); delete ctx; return GA_ERR_ARG; }
+    ctx->patches.push_back(ph);
+  }
+  char* ws = (char*)d_workspace;
+  ctx->ws = ws; ctx->ws_bytes = workspace_bytes;
+  ctx->coefM = (double*)(ws + L.off_coefM);
+  ctx->coefK = (double*)(ws + L.off_coefK);
+  ctx->chain = (double*)(ws + L.off_chain);
+  double** mv[7] = {&ctx->pred, &ctx->b, &ctx->x, &ctx->r, &ctx->z, &ctx->pv, &ctx->q};
+  for (int i = 0; i < 7; ++i) *mv[i] = (double*)(ws + L.off_mv[i]);
+  const bool multi = desc->npatch > 1;
+  ctx->mask = multi ? (unsigned char*)(ws + L.off_mask) : nullptr;
+  ctx->map = multi ? (long long*)(ws + L.off_map) : nullptr;
+  ctx->pcg = (PcgState*)(ws + L.off_pcg);
+  ctx->st = (DevStatus*)(ws + L.off_st);
+  ctx->partial = (double*)(ws + L.off_partial);
+  ctx->counter = (unsigned int*)(ws + L.off_counter);
+  ctx->dscal = (double*)(ws + L.off_dscal);
+#define CKD(call)                           \
+  do {                                      \
+    cudaError_t e_ = (call);                \
+    if (e_ != cudaSuccess) {                \
+      seterr(ctx, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+      ga_destroy(ctx);                      \
+      return GA_ERR_CUDA;                   \
+    }                                       \
+  } while (0)
+  CKD(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  CKD(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+  // zero everything small + vectors (guards must be zero/finite)
+  CKD(cudaMemsetAsync(ws + L.off_chain, 0, L.off_mask - L.off_chain, s));
+  CKD(cudaMemsetAsync(ws + L.off_pcg, 0, L.off_dscal + 256 - L.off_pcg, s));
+  if (multi) {
+    CKD(cudaMemcpyAsync(ctx->mask, sh.mask.data(), sh.g.npts, cudaMemcpyHostToDevice, s));
+    CKD(cudaMemcpyAsync(ctx->map, sh.map.data(), sizeof(long long) * sh.nfree, cudaMemcpyHostToDevice, s));
+  }
+  // assembly
+  rc = assemble(ctx, sh, (char*)d_scratch, scratch_bytes, s);
+  if (rc != GA_OK) { ga_destroy(ctx); return rc; }
+  // preconditioner: per patch 1D factors (host) and scaling s (device)
+  Tables1D T = make_tables(sh.p, sh.n);
+  std::vector<double> band = param_mass_band(T);
+  ctx->prec = sh.prec;
+  for (size_t r = 0; r < ctx->prec.size(); ++r) {
+    PrecPatch& pp = ctx->prec[r];
+    long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
+    pp.s = (double*)(ws + L.off_s[r]);
+    pp.t = multi ? (double*)(ws + L.off_t[r]) : nullptr;
+    double* dd[3] = {nullptr, nullptr, nullptr};
+    for (int d = 0; d < 3; ++d) {
+      pp.L[d] = (double*)(ws + L.off_L[d][r]);
+      if (d >= sh.dim) continue;
+      std::vector<double> Lf, diag;
+      if (!band_cholesky(band, sh.p, pp.llo[d], pp.llo[d] + pp.bd[d] - 1, Lf, diag)) {
+        seterr(ctx, "parametric mass matrix not SPD");
+        ga_destroy(ctx);
+        return GA_ERR_ARG;
+      }
+      Lf.resize((size_t)(pp.bd[d] + sh.p + 1) * (sh.p + 1), 0.0);  // P zero rows for the backward sweep
+      pp.hL[d] = Lf;
+      pp.hdiag[d] = diag;
+      CKD(cudaMemcpyAsync(pp.L[d], pp.hL[d].data(), sizeof(double) * Lf.size(), cudaMemcpyHostToDevice, s));
+      dd[d] = ctx->dscal;  // placeholder, replaced below
+    }
+    // 1D diagonals go to the t area temporarily (single patch: x MV is free now)
+    double* tmp = ctx->q;
+    size_t o = 0;
+    for (int d = 0; d < sh.dim; ++d) {
+      CKD(cudaMemcpyAsync(tmp + o, pp.hdiag[d].data(), sizeof(double) * pp.bd[d], cudaMemcpyHostToDevice, s));
+      dd[d] = tmp + o;
+      o += pp.bd[d];
+    }
+    const double* center = ctx->coefM + (ctx->S / 2) * sh.g.npts;
+    k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
+                                                                 pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
+                                                                 center, sh.g.nx, sh.g.ny, ctx->mask);
+    CKD(cudaGetLastError());
+    CKD(cudaStreamSynchronize(s));  // tmp reused by the next patch
+  }
+  CKD(cudaMemsetAsync(ctx->q, 0, sizeof(double) * sh.nvec * sh.g.padded * sh.k, s));
+  // graphs
+  // graphs are captured on a private stream (the caller's may be the legacy stream)
+  rc = build_graph(ctx, ctx->cap, GK_STEP, &ctx->gr_step, &ctx->g_step);
+  if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEK, &ctx->gr_solveK, &ctx->g_solveK);
+  if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEB, &ctx->gr_solveB, &ctx->g_solveB);
+  if (rc != GA_OK) { ga_destroy(ctx); return rc; }
+  CKD(cudaStreamSynchronize(s));
+  *out = ctx;
+  return GA_OK;
+}
+
+__global__ void k_reset_status(DevStatus* st, PcgState* pc) {
+  memset(st, 0, sizeof(DevStatus));
+  st->fail_step = -1;
+  st->fail_block = -1;
+  memset(pc, 0, sizeof(PcgState));
+}
+
+static void reset_status(ga_ctx* ctx, cudaStream_t s) { k_reset_status<<<1, 1, 0, s>>>(ctx->st, ctx->pcg); }
+
+static ga_status check_ctx(ga_ctx* ctx) {
+  if (!ctx) { seterr(nullptr, "ctx is NULL"); return GA_ERR_ARG; }
+  return GA_OK;
+}
+
+static ga_status set_predictors_and_norm(ga_ctx* ctx, cudaStream_t s) {
+  launch_predict(stage_args(ctx), s);
+  // ||U0||^2 for the instability detector
+  launch_dot(ctx->g, ctx->nvec, 1, ctx->chain, ctx->chain, &ctx->st->u0norm2, ctx->partial, ctx->counter, s);
+  CK(cudaGetLastError());
+  return GA_OK;
+}
+
+ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (!d_u0) { seterr(ctx, "u0 is NULL"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int k = ctx->k, nvec = ctx->nvec;
+  const long long vstride = (long long)nvec * ctx->g.padded;
+  reset_status(ctx, s);
+  CK(cudaMemsetAsync(ctx->chain, 0, sizeof(double) * 3 * k * vstride, s));
+  launch_api_to_grid(ctx->g, nvec, ctx->nfree, ctx->map, d_u0, ctx->chain, 1, 0, ctx->st, s);
+  if (d_v0) launch_api_to_grid(ctx->g, nvec, ctx->nfree, ctx->map, d_v0, ctx->chain + vstride, 1, 0, ctx->st, s);
+  CK(cudaGetLastError());
+  // c_m = M^{-1}(-K c_{m-2}), m = 2..3k-1, two at a time when k >= 2
+  const int batch = std::min(2, k);
+  for (int m0 = 2; m0 <= 3 * k - 1; m0 += batch) {
+    int src[KMAX] = {-1, -1, -1, -1}, dst[KMAX] = {-1, -1, -1, -1};
+    for (int j = 0; j < batch; ++j)
+      if (m0 + j <= 3 * k - 1) { src[j] = m0 + j - 2; dst[j] = m0 + j; }
+    launch_pack(ctx->g, nvec, k, ctx->chain, src, ctx->pred, ctx->st, s);
+    CK(cudaGraphLaunch(ctx->g_solveK, s));
+    launch_unpack(ctx->g, nvec, k, ctx->x, dst, ctx->chain, ctx->st, s);
+    CK(cudaGetLastError());
+  }
+  return set_predictors_and_norm(ctx, s);
+}
+
+ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (nsteps < 0) { seterr(ctx, "nsteps < 0"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int i = 0; i < nsteps; ++i) CK(cudaGraphLaunch(ctx->g_step, s));
+  return GA_OK;
+}
+
+ga_status ga_get_chain(ga_ctx* ctx, int m, double* d_out, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (m < 0 || m >= 3 * ctx->k || !d_out) { seterr(ctx, "bad chain index or NULL"); return GA_ERR_ARG; }
+  const long long vstride = (long long)ctx->nvec * ctx->g.padded;
+  launch_grid_to_api(ctx->g, ctx->nvec, ctx->nfree, ctx->map, ctx->chain + m * vstride, 1, 0, d_out, ctx->st,
+                     (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return GA_OK;
+}
+
+ga_status ga_set_chain(ga_ctx* ctx, int m, const double* d_in, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (m < 0 || m >= 3 * ctx->k || !d_in) { seterr(ctx, "bad chain index or NULL"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long vstride = (long long)ctx->nvec * ctx->g.padded;
+  if (m == 0) reset_status(ctx, s);
+  launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_in, ctx->chain + m * vstride, 1, 0, ctx->st, s);
+  CK(cudaGetLastError());
+  // predictors and ||U0|| follow the chain; cheap to refresh after every entry
+  return set_predictors_and_norm(ctx, s);
+}
+
+ga_status ga_get_state(ga_ctx* ctx, double* d_u, double* d_v, double* d_a, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  double* outs[3] = {d_u, d_v, d_a};
+  for (int m = 0; m < 3; ++m)
+    if (outs[m]) {
+      rc = ga_get_chain(ctx, m, outs[m], stream);
+      if (rc != GA_OK) return rc;
+    }
+  return GA_OK;
+}
+
+ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (!out) return GA_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevStatus h;
+  CK(cudaMemcpyAsync(&h, ctx->st, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  memset(out, 0, sizeof(*out));
+  out->steps = h.steps;
+  out->solves = h.solves;
+  for (int j = 0; j < KMAX; ++j) { out->pcg_iters[j] = h.pcg_iters[j]; out->last_iters[j] = h.last_iters[j]; }
+  out->max_iters = h.max_iters;
+  out->max_rel_residual = h.max_relres;
+  out->status = h.status;
+  out->fail_step = h.fail_step;
+  out->fail_block = h.fail_block;
+  out->kernel_launches = (long long)h.launches;
+  return GA_OK;
+}
+
+ga_status ga_apply(ga_ctx* ctx, int which, const double* d_x, double* d_y, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (which < 0 || which > 2 || !d_x || !d_y) { seterr(ctx, "bad operator or NULL"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t mvbytes = sizeof(double) * ctx->nvec * ctx->g.padded * ctx->k;
+  if (which < 2) {
+    CK(cudaMemsetAsync(ctx->pv, 0, mvbytes, s));
+    launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_x, ctx->pv, ctx->k, 0, ctx->st, s);
+    launch_spmv(spmv_args(ctx, which, ctx->pv, ctx->q, SPMV_APPLY), s);
+    launch_grid_to_api(ctx->g, ctx->nvec, ctx->nfree, ctx->map, ctx->q, ctx->k, 0, d_y, ctx->st, s);
+  } else {
+    CK(cudaMemsetAsync(ctx->r, 0, mvbytes, s));
+    CK(cudaMemsetAsync(ctx->pcg, 0, sizeof(PcgState), s));
+    launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_x, ctx->r, ctx->k, 0, ctx->st, s);
+    PrecArgs a = prec_args(ctx, 0ull, 0);
+    a.maxit = 0x7fffffff;
+    launch_precond(a, s);
+    launch_grid_to_api(ctx->g, ctx->nvec, ctx->nfree, ctx->map, ctx->z, ctx->k, 0, d_y, ctx->st, s);
+  }
+  CK(cudaGetLastError());
+  return GA_OK;
+}
+
+ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (!d_b || !d_x) { seterr(ctx, "NULL vector"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t mvbytes = sizeof(double) * ctx->nvec * ctx->g.padded * ctx->k;
+  CK(cudaMemsetAsync(ctx->b, 0, mvbytes, s));
+  launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_b, ctx->b, ctx->k, 0, ctx->st, s);
+  CK(cudaGraphLaunch(ctx->g_solveB, s));
+  launch_grid_to_api(ctx->g, ctx->nvec, ctx->nfree, ctx->map, ctx->x, ctx->k, 0, d_x, ctx->st, s);
+  CK(cudaGetLastError());
+  if (iters) {
+    PcgState h;
+    DevStatus hs;
+    CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs, ctx->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *iters = h.its[0];
+    if (hs.status != 0) return (ga_status)hs.status;
+  }
+  return GA_OK;
+}
+
+ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (iters < 1 || !lam) { seterr(ctx, "iters >= 1 and lam required"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const GridDesc& g = ctx->g;
+  const int nvec = ctx->nvec, k = ctx->k;
+  const size_t mvbytes = sizeof(double) * nvec * g.padded * k;
+  // the predictor MV is state: keep a host copy and restore it at the end
+  std::vector<double> hsave(mvbytes / sizeof(double));
+  CK(cudaMemcpyAsync(hsave.data(), ctx->pred, mvbytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemsetAsync(ctx->pred, 0, mvbytes, s));
+  const long long tot = (long long)nvec * g.npts;
+  k_altsign<<<(unsigned int)((tot + 255) / 256), 256, 0, s>>>(g, nvec, k, ctx->pred, ctx->mask);
+  double* dn = ctx->dscal;
+  for (int it = 0; it < iters; ++it) {
+    // normalise v (slot 0 of pred)
+    launch_dot(g, nvec, k, ctx->pred, ctx->pred, dn, ctx->partial, ctx->counter, s);
+    launch_scale(g, nvec, k, ctx->pred, dn, 1, s);
+    CK(cudaGraphLaunch(ctx->g_solveK, s));  // x = M^{-1}(-K v)
+    // v <- x (slot 0)
+    CK(cudaMemcpyAsync(ctx->pred, ctx->x, mvbytes, cudaMemcpyDeviceToDevice, s));
+  }
+  // Rayleigh quotient (v.Kv)/(v.Mv)
+  launch_dot(g, nvec, k, ctx->pred, ctx->pred, dn, ctx->partial, ctx->counter, s);
+  launch_scale(g, nvec, k, ctx->pred, dn, 1, s);
+  launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->q, SPMV_APPLY), s);
+  launch_dot(g, nvec, k, ctx->pred, ctx->q, dn + 1, ctx->partial, ctx->counter, s);
+  launch_spmv(spmv_args(ctx, 0, ctx->pred, ctx->q, SPMV_APPLY), s);
+  launch_dot(g, nvec, k, ctx->pred, ctx->q, dn + 2, ctx->partial, ctx->counter, s);
+  double hv[3];
+  CK(cudaMemcpyAsync(hv, dn, sizeof(hv), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->pred, hsave.data(), mvbytes, cudaMemcpyHostToDevice, s));
+  DevStatus hs;
+  CK(cudaMemcpyAsync(&hs, ctx->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *lam = hv[1] / hv[2];
+  if (hs.status != 0) return (ga_status)hs.status;
+  return GA_OK;
+}
+
+ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map) {
+  if (!ctx || !host_map) return GA_ERR_ARG;
+  memcpy(host_map, ctx->hlocal.data(), sizeof(long long) * ctx->hlocal.size());
+  return GA_OK;
+}
+
+void ga_destroy(ga_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->g_step) cudaGraphExecDestroy(ctx->g_step);
+  if (ctx->g_solveK) cudaGraphExecDestroy(ctx->g_solveK);
+  if (ctx->g_solveB) cudaGraphExecDestroy(ctx->g_solveB);
+  if (ctx->gr_step) cudaGraphDestroy(ctx->gr_step);
+  if (ctx->gr_solveK) cudaGraphDestroy(ctx->gr_solveK);
+  if (ctx->gr_solveB) cudaGraphDestroy(ctx->gr_solveB);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->cap) cudaStreamDestroy(ctx->cap);
+  delete ctx;
+}
+
+const char* ga_last_error(const ga_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  return g_thread_err.c_str();
+}
+
+}  // extern "C"

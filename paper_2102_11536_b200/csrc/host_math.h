@@ -1,0 +1,42 @@
+// Host-side (CPU) setup arithmetic of the CUDA path: knot vector, Gauss rule,
+// B-spline tables, 1D parametric mass matrices and their banded Cholesky
+// factors, generalized-alpha parameters.  Independent of oracle/ (no shared
+// code); cited to PAPER.md (P:line).
+#pragma once
+#include <vector>
+
+namespace ga {
+
+// Open uniform knot vector, n elements, degree p (maximal regularity P:811).
+std::vector<double> open_knots(int p, int n);
+
+// Gauss-Legendre nodes/weights on [-1,1] by Newton iteration on P_q (q points).
+void gauss_legendre(int q, std::vector<double>& x, std::vector<double>& w);
+
+// Values (der=0) or first derivatives (der=1) of the p+1 B-splines that are
+// non-zero on element e (global indices e..e+p) at parameter x, by the
+// Cox-de Boor recursion with 0/0 = 0.
+void local_basis(const std::vector<double>& knots, int p, int e, double x, double* val, double* der);
+
+// 1D tables at the n(p+1) Gauss points (element-major):
+//   val[q*(p+1)+a], der[...] for local function a (global e+a), wq[q] weight*jacobian.
+struct Tables1D {
+  int p = 0, n = 0, nq = 0, m = 0;
+  std::vector<double> pts, wq, val, der;
+};
+Tables1D make_tables(int p, int n);
+
+// Dense-band 1D parametric mass matrix Mh[i][i+t], t = 0..p over all m functions.
+std::vector<double> param_mass_band(const Tables1D& T);  // size m*(p+1)
+
+// Banded Cholesky of the restriction of Mh to indices [lo, hi] (inclusive).
+// Output per row i (local): L[i*(p+1)+0] = 1/L_ii, L[i*(p+1)+t] = L_{i,i-t}.
+// Also returns diag of the restricted Mh.
+bool band_cholesky(const std::vector<double>& band, int p, int lo, int hi,
+                   std::vector<double>& L, std::vector<double>& diag);
+
+// Generalized-alpha parameters (R2).
+int scheme_params(int k, double rb, double rs, int param_set,
+                  double* alpha, double* beta, double* gamma, double* alpha_f, double* theta_max);
+
+}  // namespace ga

@@ -1,0 +1,709 @@
+// Hot-path kernels of the explicit order-2k generalized-alpha step (sm_100a, fp64).
+//
+//  * k_spmv      stencil SpMV y = A x on the column-index-free layout coef[o][row]
+//                for all lock-stepped right-hand sides at once (coefficients are
+//                read once per k RHS).  Modes: apply, -A x (right-hand sides
+//                b_j = -K s_j), q = M p with the p.q reduction and the
+//                alpha update fused (PCG), r = b - M x (refinement R8).
+//  * k_line      banded Cholesky forward/backward substitution along grid lines:
+//                the Kronecker factor Mh_d^{-1} of calM^{-1}.
+//  * k_prec_*    diagonal scaling s = sqrt(Dh/D) and additive Schwarz
+//                gather / sum, with the r.z and r.r reductions fused.
+//  * k_stage     the 3k-variable update of P:408-431 (reading R1) for all blocks
+//                at once, per DoF, fused with the next step's predictors.
+#include <cuda_runtime.h>
+
+#include "ops.cuh"
+
+namespace ga {
+
+#define CUDA_LAUNCH_CHECK()
+
+// ---------------------------------------------------------------------------
+// Stencil SpMV
+// ---------------------------------------------------------------------------
+template <int KK>
+__device__ __forceinline__ void load_row(const double* __restrict__ p, double (&v)[KK]) {
+  if constexpr (KK == 2) {
+    double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = t.x; v[1] = t.y;
+  } else if constexpr (KK == 4) {
+    double2 t0 = __ldg(reinterpret_cast<const double2*>(p));
+    double2 t1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < KK; ++j) v[j] = __ldg(p + j);
+  }
+}
+
+template <int P, int NC, int KK, bool ELASTIC>
+__global__ void __launch_bounds__(NTHREADS) k_spmv(SpmvArgs a) {
+  if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
+  count_launch(a.st);
+  const GridDesc g = a.g;
+  const long long i = (long long)gtid();
+  const bool valid = i < g.npts;
+  constexpr int W = 2 * P + 1;
+  const int P3 = (g.dim == 3) ? P : 0;
+  const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+  const long long S = (long long)W * W * (g.dim == 3 ? W : 1);
+  constexpr int NA = ELASTIC ? 3 : NC;  // output component vectors
+  double acc[NA][KK];
+#pragma unroll
+  for (int c = 0; c < NA; ++c)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
+  if (valid) {
+    const double* __restrict__ coef = a.coef;
+    const double* __restrict__ x = a.x;
+    long long o = 0;
+    for (int o3 = -P3; o3 <= P3; ++o3) {
+      for (int o2 = -P; o2 <= P; ++o2) {
+        const long long rowbase = g.guard + i + o3 * sz + o2 * sy;
+#pragma unroll
+        for (int o1 = -P; o1 <= P; ++o1, ++o) {
+          const long long col = rowbase + o1;
+          if constexpr (!ELASTIC) {
+            const double cf = __ldg(coef + o * g.npts + i);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              double v[KK];
+              load_row<KK>(x + ((long long)c * g.padded + col) * KK, v);
+#pragma unroll
+              for (int j = 0; j < KK; ++j) acc[c][j] = fma(cf, v[j], acc[c][j]);
+            }
+          } else {
+            double v[3][KK];
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) load_row<KK>(x + ((long long)bb * g.padded + col) * KK, v[bb]);
+#pragma unroll
+            for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+              for (int bb = 0; bb < 3; ++bb) {
+                const double cf = __ldg(coef + ((long long)(aa * 3 + bb) * S + o) * g.npts + i);
+#pragma unroll
+                for (int j = 0; j < KK; ++j) acc[aa][j] = fma(cf, v[bb][j], acc[aa][j]);
+              }
+          }
+        }
+      }
+    }
+  }
+  // epilogue
+  double dots[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) dots[j] = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < NA; ++c) {
+      const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        double v = acc[c][j];
+        if (a.mode == SPMV_NEGB) v = -v;
+        else if (a.mode == SPMV_TRUERES) { v = a.b[base + j] - v; dots[j] = fma(v, v, dots[j]); }
+        else if (a.mode == SPMV_PQ) dots[j] = fma(a.x[base + j], v, dots[j]);
+        a.y[base + j] = v;
+      }
+    }
+  }
+  if (a.mode == SPMV_PQ) {
+    double tot[KK];
+    if (reduce_last_block<KK>(dots, a.partial, a.counter, tot)) {
+      PcgState* pc = a.pcg;
+      pc->iter += 1;
+      pc->pfirst = 0;
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        pc->pq[j] = tot[j];
+        if (pc->active[j]) {
+          pc->alpha[j] = pc->rz[j] / tot[j];
+          pc->its[j] += 1;
+        } else {
+          pc->alpha[j] = 0.0;
+        }
+      }
+    }
+  } else if (a.mode == SPMV_TRUERES) {
+    double tot[KK];
+    if (reduce_last_block<KK>(dots, a.partial, a.counter, tot)) {
+      // restart of PCG from the true residual (refinement phase, R8)
+      PcgState* pc = a.pcg;
+      pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->phase = 1;
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        pc->alpha[j] = 0.0;
+        pc->active[j] = pc->bb[j] > 0.0 ? 1 : 0;
+        double thr = a.tol2 * pc->bb[j];
+        if (a.refine_rtol2 > 0.0) thr = fmin(thr, a.refine_rtol2 * tot[j]);
+        pc->thr[j] = thr;
+      }
+    }
+  }
+}
+
+template <int P, int NC, int KK>
+static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
+  const unsigned int nb = (unsigned int)((a.g.npts + NTHREADS - 1) / NTHREADS);
+  if (a.elastic) {
+    if constexpr (NC == 3) k_spmv<P, 3, KK, true><<<nb, NTHREADS, 0, s>>>(a);
+  } else {
+    k_spmv<P, NC, KK, false><<<nb, NTHREADS, 0, s>>>(a);
+  }
+}
+template <int P, int NC>
+static void spmv_nc(const SpmvArgs& a, cudaStream_t s) {
+  switch (a.kk) {
+    case 1: spmv_kk<P, NC, 1>(a, s); break;
+    case 2: spmv_kk<P, NC, 2>(a, s); break;
+    case 3: spmv_kk<P, NC, 3>(a, s); break;
+    default: spmv_kk<P, NC, 4>(a, s); break;
+  }
+}
+template <int P>
+static void spmv_p(const SpmvArgs& a, cudaStream_t s) {
+  if (a.nvec == 3) spmv_nc<P, 3>(a, s);
+  else spmv_nc<P, 1>(a, s);
+}
+void launch_spmv(const SpmvArgs& a, cudaStream_t s) {
+  switch (a.p) {
+    case 1: spmv_p<1>(a, s); break;
+    case 2: spmv_p<2>(a, s); break;
+    case 3: spmv_p<3>(a, s); break;
+    case 4: spmv_p<4>(a, s); break;
+    case 5: spmv_p<5>(a, s); break;
+    case 6: spmv_p<6>(a, s); break;
+    default: spmv_p<7>(a, s); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Preconditioner: scaling, line solves, Schwarz sum
+// ---------------------------------------------------------------------------
+// x += alpha p, r -= alpha q (when a PCG iteration precedes), then the scaled
+// input t = s o r of the (single) patch into z, or of every patch into its box.
+__global__ void __launch_bounds__(NTHREADS) k_xr_prec_in(PrecArgs a) {
+  if (a.st->status != 0) return;
+  count_launch(a.st);
+  const GridDesc g = a.g;
+  const long long tot = (long long)a.nvec * g.npts * a.kk;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const int j = (int)(e % a.kk);
+  const long long ci = e / a.kk;
+  const long long i = ci % g.npts;
+  const int c = (int)(ci / g.npts);
+  const long long idx = ((long long)c * g.padded + g.guard + i) * a.kk + j;
+  double r = a.r[idx];
+  if (a.update && !a.pcg->first) {
+    const double al = a.pcg->alpha[j];
+    if (al != 0.0) {
+      a.x[idx] = fma(al, a.p_[idx], a.x[idx]);
+      r = fma(-al, a.q[idx], r);
+      a.r[idx] = r;
+    }
+  }
+  if (a.npatch == 1 && a.t[0] == nullptr) {
+    a.z[idx] = a.s[0][i] * r;
+  }
+}
+
+// multi-patch gather: t_r = s_r o R_r r on the box of patch r
+__global__ void __launch_bounds__(NTHREADS) k_prec_gather(PrecArgs a, int pr) {
+  if (a.st->status != 0) return;
+  count_launch(a.st);
+  const GridDesc g = a.g;
+  const int bx = a.bd[pr][0], by = a.bd[pr][1], bz = a.bd[pr][2];
+  const long long nbox = (long long)bx * by * bz;
+  const long long tot = (long long)a.nvec * nbox * a.kk;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const int j = (int)(e % a.kk);
+  const long long ci = e / a.kk;
+  const long long bi = ci % nbox;
+  const int c = (int)(ci / nbox);
+  const int ix = (int)(bi % bx), iy = (int)((bi / bx) % by), iz = (int)(bi / ((long long)bx * by));
+  const long long gi = (a.lo[pr][0] + ix) + (long long)g.nx * ((a.lo[pr][1] + iy) + (long long)g.ny * (a.lo[pr][2] + iz));
+  const double sv = a.s[pr][bi];
+  const double r = a.r[((long long)c * g.padded + g.guard + gi) * a.kk + j];
+  a.t[pr][((long long)c * nbox + bi) * a.kk + j] = sv * r;
+}
+
+// Forward then backward substitution with the banded Cholesky factor along
+// lines of length len (element stride es); one thread per (comp, line, rhs).
+template <int P>
+__global__ void __launch_bounds__(NTHREADS) k_line(double* __restrict__ t, const double* __restrict__ L, int len,
+                                                   long long es, int na, long long sa, int nb, long long sb, int kk,
+                                                   int nvec, long long sc, DevStatus* st) {
+  if (st->status != 0) return;
+  count_launch(st);
+  const long long nl = (long long)nvec * nb * na * kk;
+  const long long l = (long long)gtid();
+  if (l >= nl) return;
+  const int j = (int)(l % kk);
+  long long rem = l / kk;
+  const int ia = (int)(rem % na);
+  rem /= na;
+  const int ib = (int)(rem % nb);
+  const int c = (int)(rem / nb);
+  double* base = t + c * sc + ib * sb + ia * sa + j;
+  double y[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) y[u] = 0.0;
+  // forward: y_i = (t_i - sum_{u=1..P} L_{i,i-u} y_{i-u}) / L_ii
+  for (int i = 0; i < len; ++i) {
+    double v = base[(long long)i * es];
+    const double* Li = L + (long long)i * (P + 1);
+#pragma unroll
+    for (int u = P; u >= 1; --u) v = fma(-__ldg(Li + u), y[u - 1], v);
+    v *= __ldg(Li);
+#pragma unroll
+    for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+    y[0] = v;
+    base[(long long)i * es] = v;
+  }
+  // backward: z_i = (y_i - sum_{u=1..P} L_{i+u,i} z_{i+u}) / L_ii   (L padded with P zero rows)
+#pragma unroll
+  for (int u = 0; u < P; ++u) y[u] = 0.0;
+  for (int i = len - 1; i >= 0; --i) {
+    double v = base[(long long)i * es];
+#pragma unroll
+    for (int u = P; u >= 1; --u) v = fma(-__ldg(L + (long long)(i + u) * (P + 1) + u), y[u - 1], v);
+    v *= __ldg(L + (long long)i * (P + 1));
+#pragma unroll
+    for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+    y[0] = v;
+    base[(long long)i * es] = v;
+  }
+}
+
+template <int P>
+static void line_launch(double* t, const double* L, int len, long long es, int na, long long sa, int nb,
+                        long long sb, int kk, int nvec, long long sc, DevStatus* st, cudaStream_t s) {
+  const long long nl = (long long)nvec * nb * na * kk;
+  const unsigned int blocks = (unsigned int)((nl + NTHREADS - 1) / NTHREADS);
+  k_line<P><<<blocks, NTHREADS, 0, s>>>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st);
+}
+static void line_dispatch(int p, double* t, const double* L, int len, long long es, int na, long long sa, int nb,
+                          long long sb, int kk, int nvec, long long sc, DevStatus* st, cudaStream_t s) {
+  switch (p) {
+    case 1: line_launch<1>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+    case 2: line_launch<2>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+    case 3: line_launch<3>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+    case 4: line_launch<4>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+    case 5: line_launch<5>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+    case 6: line_launch<6>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+    default: line_launch<7>(t, L, len, es, na, sa, nb, sb, kk, nvec, sc, st, s); break;
+  }
+}
+
+// F1: convergence test, beta, loop condition (thread 0 of the last block).
+__device__ void pcg_finalize_precond(const PrecArgs& a, const double* rz, const double* rr) {
+  PcgState* pc = a.pcg;
+  DevStatus* st = a.st;
+  int any = 0;
+  for (int j = 0; j < a.kk; ++j) {
+    pc->rz[j] = rz[j];
+    pc->rr[j] = rr[j];
+    if (pc->active[j] && rr[j] <= pc->thr[j]) pc->active[j] = 0;
+    if (pc->first) {
+      pc->beta[j] = 0.0;
+    } else {
+      pc->beta[j] = pc->rzold[j] != 0.0 ? rz[j] / pc->rzold[j] : 0.0;
+    }
+    pc->rzold[j] = rz[j];
+    any |= pc->active[j];
+  }
+  if (pc->first) pc->pfirst = 1;
+  pc->first = 0;
+  int cond = any;
+  if (any && pc->iter >= a.maxit) {
+    if (st->status == 0 && pc->phase == 0) {  // the refinement phase may stop at maxit
+      st->status = -5;  // GA_ERR_NOCONV
+      st->fail_step = st->steps;
+      for (int j = 0; j < a.kk; ++j)
+        if (pc->active[j]) { st->fail_block = j; break; }
+    }
+    cond = 0;
+  }
+  if (st->status != 0) cond = 0;
+  if (a.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)a.cond, cond ? 1u : 0u);
+}
+
+// z = sum_r s_r o t_r (single patch: z *= s in place), then r.z and r.r.
+template <int KK>
+__global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
+  const bool dead = a.st->status != 0;
+  if (!dead) count_launch(a.st);
+  const GridDesc g = a.g;
+  const long long tot = (long long)a.nvec * g.npts;
+  const long long e = (long long)gtid();
+  double v[2 * KK];
+#pragma unroll
+  for (int j = 0; j < 2 * KK; ++j) v[j] = 0.0;
+  if (!dead && e < tot) {
+    const long long i = e % g.npts;
+    const int c = (int)(e / g.npts);
+    const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+    double z[KK];
+    if (a.npatch == 1 && a.t[0] == nullptr) {
+      const double sv = a.s[0][i];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) z[j] = sv * a.z[base + j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < KK; ++j) z[j] = 0.0;
+      const int ix = (int)(i % g.nx), iy = (int)((i / g.nx) % g.ny), iz = (int)(i / ((long long)g.nx * g.ny));
+      const bool free_pt = a.mask == nullptr || a.mask[i];
+      if (free_pt) {
+        for (int pr = 0; pr < a.npatch; ++pr) {
+          const int lx = ix - a.lo[pr][0], ly = iy - a.lo[pr][1], lz = iz - a.lo[pr][2];
+          if (lx < 0 || ly < 0 || lz < 0 || lx >= a.bd[pr][0] || ly >= a.bd[pr][1] || lz >= a.bd[pr][2]) continue;
+          const long long nbox = (long long)a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2];
+          const long long bi = lx + (long long)a.bd[pr][0] * (ly + (long long)a.bd[pr][1] * lz);
+          const double sv = a.s[pr][bi];
+#pragma unroll
+          for (int j = 0; j < KK; ++j) z[j] = fma(sv, a.t[pr][((long long)c * nbox + bi) * KK + j], z[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      a.z[base + j] = z[j];
+      const double r = a.r[base + j];
+      v[j] = r * z[j];
+      v[KK + j] = r * r;
+    }
+  }
+  if (dead) return;
+  double out[2 * KK];
+  if (reduce_last_block<2 * KK>(v, a.partial, a.counter, out)) {
+    double rz[KMAX], rr[KMAX];
+    for (int j = 0; j < KK; ++j) { rz[j] = out[j]; rr[j] = out[KK + j]; }
+    pcg_finalize_precond(a, rz, rr);
+  }
+}
+
+void launch_precond(const PrecArgs& a, cudaStream_t s) {
+  const GridDesc& g = a.g;
+  {
+    const long long tot = (long long)a.nvec * g.npts * a.kk;
+    k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+  }
+  const bool single = (a.npatch == 1 && a.t[0] == nullptr);
+  for (int pr = 0; pr < a.npatch; ++pr) {
+    double* t;
+    long long str[3];
+    long long sc;
+    int bd[3] = {a.bd[pr][0], a.bd[pr][1], a.bd[pr][2]};
+    if (single) {
+      t = a.z + g.guard * a.kk;
+      str[0] = a.kk; str[1] = (long long)g.nx * a.kk; str[2] = (long long)g.nx * g.ny * a.kk;
+      sc = g.padded * a.kk;
+    } else {
+      const long long nbox = (long long)bd[0] * bd[1] * bd[2];
+      k_prec_gather<<<(unsigned int)((a.nvec * nbox * a.kk + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a, pr);
+      t = a.t[pr];
+      str[0] = a.kk; str[1] = (long long)bd[0] * a.kk; str[2] = (long long)bd[0] * bd[1] * a.kk;
+      sc = nbox * a.kk;
+    }
+    for (int d = 0; d < g.dim; ++d) {
+      // the two other directions enumerate the lines (first one fastest)
+      int o1 = (d == 0) ? 1 : 0;
+      int o2 = (d == 2) ? 1 : 2;
+      int na = bd[o1], nb = (g.dim == 3) ? bd[o2] : 1;
+      long long sa = str[o1], sb = (g.dim == 3) ? str[o2] : 0;
+      line_dispatch(a.p, t, a.L[pr][d], bd[d], str[d], na, sa, nb, sb, a.kk, a.nvec, sc, a.st, s);
+    }
+  }
+  const long long tot = (long long)a.nvec * g.npts;
+  const unsigned int nb = (unsigned int)((tot + NTHREADS - 1) / NTHREADS);
+  switch (a.kk) {
+    case 1: k_prec_out<1><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 2: k_prec_out<2><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 3: k_prec_out<3><<<nb, NTHREADS, 0, s>>>(a); break;
+    default: k_prec_out<4><<<nb, NTHREADS, 0, s>>>(a); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PCG vector kernels
+// ---------------------------------------------------------------------------
+template <int KK>
+__global__ void __launch_bounds__(NTHREADS) k_init_from_b(VecArgs a) {
+  const bool dead = a.st->status != 0;
+  if (!dead) count_launch(a.st);
+  const GridDesc g = a.g;
+  const long long tot = (long long)a.nvec * g.npts;
+  const long long e = (long long)gtid();
+  double v[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) v[j] = 0.0;
+  if (!dead && e < tot) {
+    const long long i = e % g.npts;
+    const int c = (int)(e / g.npts);
+    const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      const double b = a.b[base + j];
+      a.r[base + j] = b;
+      a.x[base + j] = 0.0;
+      v[j] = b * b;
+    }
+  }
+  if (dead) return;
+  double out[KK];
+  if (reduce_last_block<KK>(v, a.partial, a.counter, out)) {
+    PcgState* pc = a.pcg;
+    pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->nrhs = KK; pc->phase = 0;
+    for (int j = 0; j < KK; ++j) {
+      pc->bb[j] = out[j];
+      pc->thr[j] = a.tol2 * out[j];
+      pc->active[j] = out[j] > 0.0 ? 1 : 0;
+      pc->its[j] = 0;
+      pc->alpha[j] = 0.0;
+      pc->beta[j] = 0.0;
+    }
+  }
+}
+void launch_init_from_b(const VecArgs& a, cudaStream_t s) {
+  const long long tot = (long long)a.nvec * a.g.npts;
+  const unsigned int nb = (unsigned int)((tot + NTHREADS - 1) / NTHREADS);
+  switch (a.kk) {
+    case 1: k_init_from_b<1><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 2: k_init_from_b<2><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 3: k_init_from_b<3><<<nb, NTHREADS, 0, s>>>(a); break;
+    default: k_init_from_b<4><<<nb, NTHREADS, 0, s>>>(a); break;
+  }
+}
+
+// p = z (first iteration of a phase) or p = z + beta p, for active blocks.
+__global__ void __launch_bounds__(NTHREADS) k_p_update(VecArgs a) {
+  if (a.st->status != 0) return;
+  count_launch(a.st);
+  const GridDesc g = a.g;
+  const long long tot = (long long)a.nvec * g.npts * a.kk;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const int j = (int)(e % a.kk);
+  if (!a.pcg->active[j]) return;
+  const long long ci = e / a.kk;
+  const long long i = ci % g.npts;
+  const int c = (int)(ci / g.npts);
+  const long long idx = ((long long)c * g.padded + g.guard + i) * a.kk + j;
+  const double z = a.z[idx];
+  a.p[idx] = a.pcg->pfirst ? z : fma(a.pcg->beta[j], a.p[idx], z);
+}
+void launch_p_update(const VecArgs& a, cudaStream_t s) {
+  const long long tot = (long long)a.nvec * a.g.npts * a.kk;
+  k_p_update<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+}
+
+__global__ void k_solve_end(PcgState* pc, DevStatus* st) {
+  count_launch(st);
+  if (threadIdx.x != 0) return;
+  long long ns = 0;
+  for (int j = 0; j < pc->nrhs; ++j) {
+    if (pc->bb[j] > 0.0) {
+      ++ns;
+      st->pcg_iters[j] += pc->its[j];
+      st->last_iters[j] = pc->its[j];
+      if (pc->its[j] > st->max_iters) st->max_iters = pc->its[j];
+      double rel = sqrt(pc->rr[j] / pc->bb[j]);
+      if (rel > st->max_relres) st->max_relres = rel;
+    } else {
+      st->last_iters[j] = 0;
+    }
+  }
+  st->solves += ns;
+}
+void launch_solve_end(PcgState* pcg, DevStatus* st, cudaStream_t s) { k_solve_end<<<1, 32, 0, s>>>(pcg, st); }
+
+// ---------------------------------------------------------------------------
+// Stage update (reading R1): one thread per (component, DoF)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double taylor(const double* c, int m, int n3k, const double* f) {
+  double s = 0.0;
+  for (int i = n3k - 1 - m; i >= 0; --i) s = fma(f[i], c[m + i], s);
+  return s;
+}
+
+template <bool STEP>
+__global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
+  const bool dead = a.st->status != 0;
+  if (!dead) count_launch(a.st);
+  const GridDesc g = a.g;
+  const int k = a.k, n3 = 3 * a.k;
+  const long long tot = (long long)a.nvec * g.npts;
+  const long long e = (long long)gtid();
+  double u2[1] = {0.0};
+  if (!dead && e < tot) {
+    const long long i = e % g.npts;
+    const int c = (int)(e / g.npts);
+    const long long vstride = (long long)a.nvec * g.padded;
+    const long long off = (long long)c * g.padded + g.guard + i;
+    double cc[3 * KMAX], nw[3 * KMAX];
+    for (int m = 0; m < n3; ++m) cc[m] = a.chain[m * vstride + off];
+    if (STEP) {
+      const long long yb = ((long long)c * g.padded + g.guard + i) * k;
+      for (int j = 0; j < k; ++j) {
+        const int d = 3 * j, v = 3 * j + 1, ac = 3 * j + 2;
+        const double Td = taylor(cc, d, n3, a.f), Tv = taylor(cc, v, n3, a.f), Ta = taylor(cc, ac, n3, a.f);
+        const double P = (a.ysol[yb + j] - Ta) / a.alpha[j];
+        nw[d] = fma(a.beta[j] * a.tau * a.tau, P, Td);
+        nw[v] = fma(a.gamma[j] * a.tau, P, Tv);
+        nw[ac] = Ta + P;
+      }
+      for (int m = 0; m < n3; ++m) a.chain[m * vstride + off] = nw[m];
+    } else {
+      for (int m = 0; m < n3; ++m) nw[m] = cc[m];
+    }
+    // predictors of the next step: s_j = T_disp(c) (j < k), s_k = c_{3k-3}
+    const long long pb = ((long long)c * g.padded + g.guard + i) * k;
+    for (int j = 0; j < k; ++j) {
+      const int d = 3 * j;
+      a.pred[pb + j] = (j < k - 1) ? taylor(nw, d, n3, a.f) : nw[d];
+    }
+    u2[0] = nw[0] * nw[0];
+  }
+  if (dead || !STEP) return;
+  double out[1];
+  if (reduce_last_block<1>(u2, a.partial, a.counter, out)) {
+    DevStatus* st = a.st;
+    st->steps += 1;
+    if (a.unstable2 > 0.0 && !(out[0] <= a.unstable2 * st->u0norm2)) {
+      st->status = -6;  // GA_ERR_UNSTABLE
+      st->fail_step = st->steps;
+      st->fail_block = -1;
+    }
+  }
+}
+void launch_stage(const StageArgs& a, cudaStream_t s) {
+  const long long tot = (long long)a.nvec * a.g.npts;
+  k_stage<true><<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+}
+void launch_predict(const StageArgs& a, cudaStream_t s) {
+  const long long tot = (long long)a.nvec * a.g.npts;
+  k_stage<false><<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// Packing / copies / small reductions
+// ---------------------------------------------------------------------------
+struct Idx4 { int v[KMAX]; };
+
+__global__ void k_pack(GridDesc g, int nvec, int kk, const double* chain, Idx4 src, double* mv, DevStatus* st) {
+  count_launch(st);
+  const long long tot = (long long)nvec * g.npts * kk;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const int j = (int)(e % kk);
+  const long long ci = e / kk;
+  const long long i = ci % g.npts;
+  const int c = (int)(ci / g.npts);
+  const long long vstride = (long long)nvec * g.padded;
+  const double v = src.v[j] >= 0 ? chain[src.v[j] * vstride + (long long)c * g.padded + g.guard + i] : 0.0;
+  mv[((long long)c * g.padded + g.guard + i) * kk + j] = v;
+}
+__global__ void k_unpack(GridDesc g, int nvec, int kk, const double* mv, Idx4 dst, double* chain, DevStatus* st) {
+  count_launch(st);
+  const long long tot = (long long)nvec * g.npts * kk;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const int j = (int)(e % kk);
+  if (dst.v[j] < 0) return;
+  const long long ci = e / kk;
+  const long long i = ci % g.npts;
+  const int c = (int)(ci / g.npts);
+  const long long vstride = (long long)nvec * g.padded;
+  chain[dst.v[j] * vstride + (long long)c * g.padded + g.guard + i] = mv[((long long)c * g.padded + g.guard + i) * kk + j];
+}
+void launch_pack(const GridDesc& g, int nvec, int kk, const double* chain, const int* src, double* mv,
+                 DevStatus* st, cudaStream_t s) {
+  Idx4 ix;
+  for (int j = 0; j < KMAX; ++j) ix.v[j] = j < kk ? src[j] : -1;
+  const long long tot = (long long)nvec * g.npts * kk;
+  k_pack<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, chain, ix, mv, st);
+}
+void launch_unpack(const GridDesc& g, int nvec, int kk, const double* mv, const int* dst, double* chain,
+                   DevStatus* st, cudaStream_t s) {
+  Idx4 ix;
+  for (int j = 0; j < KMAX; ++j) ix.v[j] = j < kk ? dst[j] : -1;
+  const long long tot = (long long)nvec * g.npts * kk;
+  k_unpack<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, mv, ix, chain, st);
+}
+
+// api[c*nfree + f] <-> grid[((c*padded + guard + map[f]) * kk + slot)]
+__global__ void k_api_to_grid(GridDesc g, int nvec, long long nfree, const long long* map, const double* api,
+                              double* gv, int kk, int slot, DevStatus* st) {
+  count_launch(st);
+  const long long tot = (long long)nvec * nfree;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const long long f = e % nfree;
+  const int c = (int)(e / nfree);
+  const long long gi = map ? map[f] : f;
+  gv[((long long)c * g.padded + g.guard + gi) * kk + slot] = api[e];
+}
+__global__ void k_grid_to_api(GridDesc g, int nvec, long long nfree, const long long* map, const double* gv, int kk,
+                              int slot, double* api, DevStatus* st) {
+  count_launch(st);
+  const long long tot = (long long)nvec * nfree;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const long long f = e % nfree;
+  const int c = (int)(e / nfree);
+  const long long gi = map ? map[f] : f;
+  api[e] = gv[((long long)c * g.padded + g.guard + gi) * kk + slot];
+}
+void launch_api_to_grid(const GridDesc& g, int nvec, long long nfree, const long long* map, const double* api,
+                        double* gridv, int kk, int slot, DevStatus* st, cudaStream_t s) {
+  const long long tot = (long long)nvec * nfree;
+  if (tot == 0) return;
+  k_api_to_grid<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, nfree, map, api, gridv,
+                                                                                   kk, slot, st);
+}
+void launch_grid_to_api(const GridDesc& g, int nvec, long long nfree, const long long* map, const double* gridv,
+                        int kk, int slot, double* api, DevStatus* st, cudaStream_t s) {
+  const long long tot = (long long)nvec * nfree;
+  if (tot == 0) return;
+  k_grid_to_api<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, nfree, map, gridv, kk,
+                                                                                   slot, api, st);
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_dot(GridDesc g, int nvec, int kk, const double* a, const double* b,
+                                                  double* outp, double* partial, unsigned int* counter) {
+  const long long tot = (long long)nvec * g.npts;
+  const long long e = (long long)gtid();
+  double v[1] = {0.0};
+  if (e < tot) {
+    const long long i = e % g.npts;
+    const int c = (int)(e / g.npts);
+    const long long idx = ((long long)c * g.padded + g.guard + i) * kk;
+    v[0] = a[idx] * b[idx];
+  }
+  double out[1];
+  if (reduce_last_block<1>(v, partial, counter, out)) *outp = out[0];
+}
+void launch_dot(const GridDesc& g, int nvec, int kk, const double* a, const double* b, double* out, double* partial,
+                unsigned int* counter, cudaStream_t s) {
+  const long long tot = (long long)nvec * g.npts;
+  k_dot<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, a, b, out, partial, counter);
+}
+__global__ void k_scale(GridDesc g, int nvec, int kk, double* a, const double* num, int inv_sqrt) {
+  const long long tot = (long long)nvec * g.npts;
+  const long long e = (long long)gtid();
+  if (e >= tot) return;
+  const long long i = e % g.npts;
+  const int c = (int)(e / g.npts);
+  const long long idx = ((long long)c * g.padded + g.guard + i) * kk;
+  const double sc = inv_sqrt ? 1.0 / sqrt(*num) : *num;
+  a[idx] *= sc;
+}
+void launch_scale(const GridDesc& g, int nvec, int kk, double* a, const double* num, int inv_sqrt, cudaStream_t s) {
+  const long long tot = (long long)nvec * g.npts;
+  k_scale<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, a, num, inv_sqrt);
+}
+
+}  // namespace ga

@@ -1,0 +1,107 @@
+// Hot-path kernels (stencil SpMV, Kronecker line solves, PCG vector ops,
+// stage update) — declarations of the host-side launchers.
+#pragma once
+#include "common.cuh"
+
+namespace ga {
+
+enum SpmvMode { SPMV_APPLY = 0, SPMV_NEGB = 1, SPMV_PQ = 2, SPMV_TRUERES = 3 };
+
+// Multi-vector (MV) layout: element (comp c, grid point i, rhs j) at
+//   ((c * padded + guard + i) * kk + j)
+struct SpmvArgs {
+  const double* coef;  // scalar: [S][npts]; elastic: [9][S][npts]
+  const double* x;
+  double* y;
+  const double* b;     // SPMV_TRUERES
+  GridDesc g;
+  int nvec;            // component vectors per MV (1 or 3)
+  int kk;              // rhs per MV
+  int p;
+  int elastic;         // 1: 3x3 block stencil
+  int mode;
+  double tol2, refine_rtol2;  // SPMV_TRUERES: thresholds of the refinement phase
+  PcgState* pcg;
+  DevStatus* st;
+  double* partial;
+  unsigned int* counter;
+};
+void launch_spmv(const SpmvArgs& a, cudaStream_t s);
+
+struct PrecArgs {
+  GridDesc g;
+  int nvec, kk, p;
+  int npatch;
+  // per patch box in grid coordinates
+  int lo[MAXPATCH][3];
+  int bd[MAXPATCH][3];
+  const double* s[MAXPATCH];      // scaling sqrt(Dh/D) on the box (0 on masked points)
+  double* t[MAXPATCH];            // box work arrays [c][box][kk] (single patch: nullptr, uses z)
+  const double* L[MAXPATCH][3];   // banded Cholesky factors per direction, (len+p) rows of p+1
+  const unsigned char* mask;      // grid mask (nullptr: all free)
+  // PCG vectors (MV)
+  double *x, *r, *z;
+  const double *p_, *q;
+  PcgState* pcg;
+  DevStatus* st;
+  double* partial;
+  unsigned int* counter;          // 1 site
+  double tol2;
+  int maxit;
+  unsigned long long cond;        // graph conditional handle (0: none)
+  int update;                     // apply x += alpha p, r -= alpha q first (if !pcg->first)
+};
+void launch_precond(const PrecArgs& a, cudaStream_t s);
+
+struct VecArgs {
+  GridDesc g;
+  int nvec, kk;
+  double tol2;
+  double *x, *r, *z, *p, *b;
+  PcgState* pcg;
+  DevStatus* st;
+  double* partial;
+  unsigned int* counter;
+};
+void launch_init_from_b(const VecArgs& a, cudaStream_t s);
+void launch_p_update(const VecArgs& a, cudaStream_t s);
+void launch_solve_end(PcgState* pcg, DevStatus* st, cudaStream_t s);
+
+struct StageArgs {
+  GridDesc g;
+  int nvec, k;
+  double* chain;        // [3k][nvec][padded]
+  const double* ysol;   // MV (x of the solve), kk = k
+  double* pred;         // MV, kk = k
+  double alpha[KMAX], beta[KMAX], gamma[KMAX];
+  double f[3 * KMAX];   // tau^i / i!
+  double tau;
+  double unstable2;     // threshold on ||U||^2 / ||U0||^2 (0: off)
+  DevStatus* st;
+  double* partial;
+  unsigned int* counter;
+};
+void launch_stage(const StageArgs& a, cudaStream_t s);
+
+// Predictors from the chain (after set_state / set_chain), same rule as the stage kernel.
+void launch_predict(const StageArgs& a, cudaStream_t s);
+
+// chain <-> MV slot packing for the initial chain (src/dst < 0: zero / skip).
+void launch_pack(const GridDesc& g, int nvec, int kk, const double* chain, const int* src, double* mv,
+                 DevStatus* st, cudaStream_t s);
+void launch_unpack(const GridDesc& g, int nvec, int kk, const double* mv, const int* dst, double* chain,
+                   DevStatus* st, cudaStream_t s);
+
+// free-DoF (API) vector <-> grid vector (stride kk, slot j) with optional map
+void launch_api_to_grid(const GridDesc& g, int nvec, long long nfree, const long long* map, const double* api,
+                        double* gridv, int kk, int slot, DevStatus* st, cudaStream_t s);
+void launch_grid_to_api(const GridDesc& g, int nvec, long long nfree, const long long* map, const double* gridv,
+                        int kk, int slot, double* api, DevStatus* st, cudaStream_t s);
+
+// dot products of MV slot 0 of two grid vectors (stride kk) into out[0] (device), via partials.
+void launch_dot(const GridDesc& g, int nvec, int kk, const double* a, const double* b, double* out,
+                double* partial, unsigned int* counter, cudaStream_t s);
+void launch_scale(const GridDesc& g, int nvec, int kk, double* a, const double* num, int inv_sqrt,
+                  cudaStream_t s);
+
+}  // namespace ga

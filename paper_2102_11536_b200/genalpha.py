@@ -1,0 +1,231 @@
+"""ctypes binding of libgenalpha.so (include/genalpha.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+library.  PyTorch supplies device memory (workspace, scratch, vectors) and the
+stream.  Importing this module on a machine without the built library raises:
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, byref, c_double, c_int, c_longlong, c_size_t, c_void_p
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgenalpha.so")
+
+GA_OK, GA_ERR_ARG, GA_ERR_PARAM, GA_ERR_GEOMETRY, GA_ERR_CONFORMITY = 0, -1, -2, -3, -4
+GA_ERR_NOCONV, GA_ERR_UNSTABLE, GA_ERR_CUDA, GA_ERR_OOM = -5, -6, -7, -8
+STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GEOMETRY",
+                -4: "GA_ERR_CONFORMITY", -5: "GA_ERR_NOCONV", -6: "GA_ERR_UNSTABLE",
+                -7: "GA_ERR_CUDA", -8: "GA_ERR_OOM"}
+
+EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_advance", "ga_get_state",
+            "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
+            "ga_lambda_max", "ga_free_dof_map", "ga_destroy", "ga_last_error"]
+
+
+class ga_patch(ctypes.Structure):
+    _fields_ = [("cell", c_int * 3), ("ctrl", POINTER(c_double))]
+
+
+class ga_desc(ctypes.Structure):
+    _fields_ = [("dim", c_int), ("ncomp", c_int), ("p", c_int), ("n", c_int), ("npatch", c_int),
+                ("patches", POINTER(ga_patch)), ("omega", c_double), ("lame_lambda", c_double),
+                ("lame_mu", c_double), ("density", c_double), ("k", c_int), ("rho_b", c_double),
+                ("rho_s", c_double), ("param_set", c_int), ("dt", c_double), ("pcg_rtol", c_double),
+                ("pcg_maxit", c_int), ("pcg_refine", c_int), ("pcg_refine_rtol", c_double),
+                ("unstable_factor", c_double)]
+
+
+class ga_stats(ctypes.Structure):
+    _fields_ = [("steps", c_longlong), ("solves", c_longlong), ("pcg_iters", c_longlong * 4),
+                ("last_iters", c_int * 4), ("max_iters", c_int), ("max_rel_residual", c_double),
+                ("status", c_int), ("fail_step", c_longlong), ("fail_block", c_int),
+                ("kernel_launches", c_longlong)]
+
+
+class GAError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2102_11536_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, D = POINTER(c_double), POINTER(ga_desc)
+    sig = {
+        "ga_params": (c_int, [c_int, c_double, c_double, c_int, P, P, P, P, P]),
+        "ga_query": (c_int, [D, POINTER(c_size_t), POINTER(c_size_t), POINTER(c_size_t), POINTER(c_size_t)]),
+        "ga_create": (c_int, [D, c_void_p, c_size_t, c_void_p, c_size_t, c_void_p, POINTER(c_void_p)]),
+        "ga_set_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+        "ga_advance": (c_int, [c_void_p, c_int, c_void_p]),
+        "ga_get_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+        "ga_get_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+        "ga_set_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+        "ga_get_stats": (c_int, [c_void_p, POINTER(ga_stats), c_void_p]),
+        "ga_apply": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+        "ga_solve_mass": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int), c_void_p]),
+        "ga_lambda_max": (c_int, [c_void_p, c_int, P, c_void_p]),
+        "ga_free_dof_map": (c_int, [c_void_p, POINTER(c_longlong)]),
+        "ga_destroy": (None, [c_void_p]),
+        "ga_last_error": (ctypes.c_char_p, [c_void_p]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+lib = _load()
+
+
+def _err(ctx=None):
+    return lib.ga_last_error(ctx).decode(errors="replace")
+
+
+def _check(code, ctx=None):
+    if code != GA_OK:
+        raise GAError(code, _err(ctx))
+
+
+# --------------------------------------------------------------------------- raw calls
+def ga_params(k, rho_b, rho_s=None, param_set=0):
+    """(alpha, beta, gamma, alpha_f, theta_max) of the k blocks (host only)."""
+    rho_s = rho_b if rho_s is None else rho_s
+    arr = [(c_double * 4)() for _ in range(4)]
+    th = c_double()
+    _check(lib.ga_params(k, rho_b, rho_s, param_set, *arr, byref(th)))
+    return tuple(np.array(a[:k]) for a in arr) + (th.value,)
+
+
+def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3, param_set=0,
+              omega=1.0, lam=1.0, mu=1.0, density=1.0, pcg_rtol=1e-13, pcg_maxit=500,
+              pcg_refine=1, pcg_refine_rtol=None, unstable_factor=1e6):
+    """ga_desc from [(cell, ctrl ndarray (m^dim, dim))].  Keeps the ctrl arrays
+    alive on the returned object (`_keep`)."""
+    arr = (ga_patch * len(patches))()
+    keep = []
+    for i, (cell, ctrl) in enumerate(patches):
+        c = np.ascontiguousarray(ctrl, dtype=np.float64)
+        keep.append(c)
+        cc = list(cell) + [0] * (3 - len(cell))
+        arr[i].cell = (c_int * 3)(*cc)
+        arr[i].ctrl = c.ctypes.data_as(POINTER(c_double))
+    d = ga_desc(dim=dim, ncomp=ncomp, p=p, n=n, npatch=len(patches), patches=arr, omega=omega,
+                lame_lambda=lam, lame_mu=mu, density=density, k=k, rho_b=rho,
+                rho_s=rho if rho_s is None else rho_s, param_set=param_set, dt=dt,
+                pcg_rtol=pcg_rtol, pcg_maxit=pcg_maxit, pcg_refine=pcg_refine,
+                pcg_refine_rtol=(1e-3 if p >= 5 else 0.0) if pcg_refine_rtol is None else pcg_refine_rtol,
+                unstable_factor=unstable_factor)
+    d._keep = (arr, keep)
+    return d
+
+
+def ga_query(desc):
+    nf, ws, sc, sm = c_size_t(), c_size_t(), c_size_t(), c_size_t()
+    _check(lib.ga_query(byref(desc), byref(nf), byref(ws), byref(sc), byref(sm)))
+    return nf.value, ws.value, sc.value, sm.value
+
+
+# --------------------------------------------------------------------------- torch-backed context
+class Context:
+    """Owns the torch-allocated workspace of one ga_ctx.  All vectors are
+    torch float64 CUDA tensors of length n_free (free-DoF order)."""
+
+    def __init__(self, desc, device="cuda", scratch_bytes=None, stream=None):
+        import torch
+        self.torch = torch
+        self.desc = desc
+        self.n_free, ws, sc, smin = ga_query(desc)
+        if scratch_bytes is not None:
+            sc = max(smin, scratch_bytes)
+        self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=device)
+        scratch = torch.empty(sc + 256, dtype=torch.uint8, device=device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        ctx = c_void_p()
+        code = lib.ga_create(byref(desc), _aligned(self.workspace), ws, _aligned(scratch), sc,
+                             c_void_p(self.stream.cuda_stream), byref(ctx))
+        del scratch
+        if code != GA_OK:
+            raise GAError(code, _err(None))
+        self.ctx = ctx
+        self.k = desc.k
+
+    def _s(self):
+        return c_void_p(self.stream.cuda_stream)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.ga_destroy(self.ctx)
+            self.ctx = None
+
+    __del__ = close
+
+    def vec(self):
+        return self.torch.zeros(self.n_free, dtype=self.torch.float64, device=self.workspace.device)
+
+    def set_state(self, u0, v0=None):
+        _check(lib.ga_set_state(self.ctx, _ptr(u0), _ptr(v0) if v0 is not None else None, self._s()), self.ctx)
+
+    def advance(self, nsteps):
+        _check(lib.ga_advance(self.ctx, int(nsteps), self._s()), self.ctx)
+
+    def get_state(self):
+        u, v, a = self.vec(), self.vec(), self.vec()
+        _check(lib.ga_get_state(self.ctx, _ptr(u), _ptr(v), _ptr(a), self._s()), self.ctx)
+        return u, v, a
+
+    def get_chain(self, m):
+        out = self.vec()
+        _check(lib.ga_get_chain(self.ctx, m, _ptr(out), self._s()), self.ctx)
+        return out
+
+    def set_chain(self, m, x):
+        _check(lib.ga_set_chain(self.ctx, m, _ptr(x), self._s()), self.ctx)
+
+    def stats(self):
+        st = ga_stats()
+        _check(lib.ga_get_stats(self.ctx, byref(st), self._s()), self.ctx)
+        return st
+
+    def apply(self, which, x):
+        y = self.vec()
+        _check(lib.ga_apply(self.ctx, {"M": 0, "K": 1, "Pinv": 2}.get(which, which), _ptr(x), _ptr(y),
+                            self._s()), self.ctx)
+        return y
+
+    def solve_mass(self, b, want_iters=True):
+        x = self.vec()
+        it = c_int(-1)
+        code = lib.ga_solve_mass(self.ctx, _ptr(b), _ptr(x), byref(it) if want_iters else None, self._s())
+        _check(code, self.ctx)
+        return x, it.value
+
+    def lambda_max(self, iters=50):
+        lam = c_double()
+        _check(lib.ga_lambda_max(self.ctx, iters, byref(lam), self._s()), self.ctx)
+        return lam.value
+
+    def free_dof_map(self):
+        ncomp = self.desc.ncomp
+        out = (c_longlong * (self.n_free // ncomp))()
+        _check(lib.ga_free_dof_map(self.ctx, out))
+        return np.frombuffer(out, dtype=np.int64).copy()
+
+
+def _aligned(t):
+    base = t.data_ptr()
+    return c_void_p((base + 255) & ~255)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    assert t.is_cuda and t.dtype.__str__() == "torch.float64" and t.is_contiguous()
+    return c_void_p(t.data_ptr())
