@@ -1,0 +1,380 @@
+"""Benchmark of the explicit order-2k generalized-alpha hot path on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2] [--p P] [--n N] [--k K] [--rho R]
+
+A "step" is one explicit step of the integrator: the K stencil
+apply on the k predictors, k lock-stepped PCG mass solves (with refinement)
+and the 3k-variable stage update, on one synthetic problem resident in HBM.
+Default workload: BASELINE.json configs[1] (2D p=3, 256x256 elements,
++-0.2h deformed patch, k=2, rho=0, dt = 0.8 CFL).  Other configs print their
+own line.
+
+Metric: DoF-updates/s = N_free x steps / device time.  Timing: W untimed
+warm-up steps, then K steps each bracketed by CUDA events on the launching
+stream, with L2 flushed (256 MiB write) between steps, barrier + synchronize
+on both sides, max over ranks.  Multi-GPU: independent replicas (the path
+does not shard), value = sum of all ranks' DoF-updates
+/ max time.  --impl reference times the CPU oracle (oracle/, as it stands) on
+rank 0 instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DoF-updates/s per explicit step (fp64, k PCG solves)"
+UNIT = "DoF-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--p", type=int)
+    ap.add_argument("--n", type=int)
+    ap.add_argument("--k", type=int)
+    ap.add_argument("--rho", type=float)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    return ap.parse_args()
+
+
+def make_cfg(args):
+    import synth
+    over = {k: getattr(args, k) for k in ("p", "n", "k", "rho") if getattr(args, k) is not None}
+    return synth.config(args.config, **over)
+
+
+def workload_name(cfg):
+    shape = "L-shape 3 patches" if cfg.get("lshape") else ("unit square" if cfg["dim"] == 2 else "unit cube")
+    kind = "elasticity" if cfg.get("ncomp", 1) > 1 else "scalar wave"
+    return (f"{cfg['name']}: {cfg['dim']}D {kind}, {shape}, p={cfg['p']}, n={cfg['n']} elements/dir, "
+            f"+-{cfg['noise']}h control-point noise (seed {cfg['seed']}), k={cfg['k']}, rho={cfg['rho']}, "
+            f"dt={cfg['cfl_frac']} CFL")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        sms = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- CPU oracle timing
+def oracle_timing(cfg, nsteps, warmup=0):
+    """Time the oracle (oracle/, as it stands) on this host: setup excluded,
+    then `warmup` untimed and `nsteps` timed steps.  Single-threaded SciPy."""
+    import numpy as np
+
+    import synth
+    from oracle import assembly, integrator
+    prob = synth.make_problem(cfg)
+    nc = cfg.get("ncomp", 1)
+    mat = dict(lam=cfg.get("lam", 1.0), mu=cfg.get("mu", 1.0), density=cfg.get("density", 1.0)) if nc > 1 else {}
+    t0 = time.perf_counter()
+    d = assembly.Discretization(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, **mat)
+    it = integrator.Integrator(d.M, d.K, cfg["k"], cfg["rho"], 1e-4)
+    t_setup = time.perf_counter() - t0
+    u0 = d.restrict_local(prob["u0"])
+    c = it.init(u0, np.zeros_like(u0))
+    for _ in range(warmup):
+        c = it.step(c)
+    t0 = time.perf_counter()
+    for _ in range(nsteps):
+        c = it.step(c)
+    t = time.perf_counter() - t0
+    return dict(n_free=d.nfree * nc, seconds=t, setup_s=t_setup, steps=nsteps)
+
+
+def cpu_cores_used():
+    return 1  # SuperLU triangular solves and SciPy CSR matvec are single-threaded
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = make_cfg(args)
+    steps, warm = args.steps, args.warmup
+    # bound the run to a few minutes: time K steps only if they fit, else a prefix
+    probe = oracle_timing(cfg, 1, 0)
+    per = probe["seconds"]
+    kmax = max(1, int(150.0 / max(per, 1e-6)))
+    k_eff = min(steps, kmax)
+    w_eff = min(warm, max(0, int(30.0 / max(per, 1e-6))))
+    r = oracle_timing(cfg, k_eff, w_eff)
+    value = r["n_free"] * r["steps"] / r["seconds"]
+    sample = (f"{r['steps']} timed steps (+{w_eff} warm-up) of the {cfg['name']} workload after "
+              f"{r['setup_s']:.1f}s untimed setup (assembly + sparse LU); steps requested {steps}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": r["steps"], "warmup": w_eff, "ms_per_step": 1e3 * r["seconds"] / r["steps"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "n_free": r["n_free"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
+                         "sample": sample, "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def algorithmic_bytes(op, ctx_info):
+    """Algorithmic (compulsory) bytes per launch, DESIGN.md "Roofline":
+    op 0 M SpMV + p.q: S coefficients per row (shared by the k RHS), read p, write q.
+    op 1 K SpMV: S (x9 elastic) coefficients per row, read s, write b.
+    op 2 preconditioner: read r, write z, read s twice, d line passes of read+write.
+    op 3 predictor pass: read 3k chain values, write k predictors."""
+    N, S, nv, k, d = ctx_info["npts"], ctx_info["S"], ctx_info["nvec"], ctx_info["k"], ctx_info["dim"]
+    if op == 0:
+        return 8 * S * N + 16 * nv * k * N
+    if op == 1:
+        return 8 * S * N * (9 if nv == 3 else 1) + 16 * nv * k * N
+    if op == 2:
+        return 16 * nv * k * N * (1 + d) + 16 * N
+    return 8 * nv * N * (3 * k + k)
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2102_11536_b200 import Context, ga_params, make_desc
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = make_cfg(args)
+    prob = synth.make_problem(cfg)
+    nc = cfg.get("ncomp", 1)
+    mat = dict(lam=cfg.get("lam", 1.0), mu=cfg.get("mu", 1.0), density=cfg.get("density", 1.0)) if nc > 1 else {}
+    _, _, _, _, thmax = ga_params(cfg["k"], cfg["rho"])
+    # dt from the GPU's own lambda_max estimate (power iteration through the library)
+    probe = Context(make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, k=cfg["k"], rho=cfg["rho"],
+                              dt=1e-6, **mat), device=dev)
+    lam = probe.lambda_max(60)
+    probe.close()
+    del probe
+    dt = cfg["cfl_frac"] * math.sqrt(thmax / lam)
+    desc = make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, k=cfg["k"], rho=cfg["rho"], dt=dt,
+                     **mat)
+    ctx = Context(desc, device=dev)
+    stream = ctx.stream
+    fmap = ctx.free_dof_map()
+    m = cfg["n"] + cfg["p"]
+    mpow = m ** cfg["dim"]
+    u0_np = np.concatenate([np.array([prob["u0"][int(v // mpow)][int(v % mpow), c] for v in fmap])
+                            for c in range(nc)])
+    u0 = torch.tensor(u0_np, dtype=torch.float64, device=dev)
+    ctx.set_state(u0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        ctx.advance(1)
+        flush.zero_()
+    torch.cuda.synchronize()
+    st0 = ctx.stats()
+    if st0.status != 0:
+        raise RuntimeError(f"warm-up failed: status {st0.status}")
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for e0, e1 in evs:
+        e0.record(stream)
+        ctx.advance(1)
+        e1.record(stream)
+        flush.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    st1 = ctx.stats()
+    if st1.status != 0:
+        raise RuntimeError(f"timed run failed: status {st1.status}")
+    launches = st1.kernel_launches - st0.kernel_launches
+    loop_iters = st1.loop_iters - st0.loop_iters
+    solves = st1.solves - st0.solves
+    its = sum(st1.pcg_iters[j] - st0.pcg_iters[j] for j in range(4))
+    n_free = ctx.n_free
+    t_max = ms
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(t.item())
+    value = world * n_free * args.steps / (t_max * 1e-3)
+
+    # ---- per-kernel timing (events on the launching stream, L2 flushed before each launch)
+    info = dict(npts=n_free // nc if not cfg.get("lshape") else None, S=(2 * cfg["p"] + 1) ** cfg["dim"], nvec=nc,
+                k=cfg["k"], dim=cfg["dim"])
+    # grid points (incl. masked) for the multi-patch layout
+    G = [(max(c[d] for c, _ in prob["patches"]) + 1) * (m - 1) - 1 for d in range(cfg["dim"])]
+    info["npts"] = int(np.prod(G))
+    kern = {}
+    names = {0: "k_spmv(M)+p.q", 1: "k_spmv(K)", 2: "preconditioner (k_xr_prec_in + k_line x d + k_prec_out)",
+             3: "k_stage(predictor pass)"}
+    for op in range(4):
+        durs = []
+        for _ in range(args.kernel_reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.profile_op(op, 1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            durs.append(e0.elapsed_time(e1))
+        avg = sum(durs) / len(durs)
+        kern[op] = dict(name=names[op], ms=avg, bytes=algorithmic_bytes(op, info))
+    steps = args.steps
+    per_step_launches = {0: loop_iters / steps, 1: 1.0, 2: (loop_iters + 2 * solves / max(1, cfg["k"])) / steps,
+                         3: 1.0}
+    share = {op: kern[op]["ms"] * per_step_launches[op] / (ms / steps) for op in kern}
+    dom = max(share, key=lambda o: share[o])
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = kern[dom]["bytes"] / (kern[dom]["ms"] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{cfg['name']}_p{cfg['p']}_n{cfg['n']}_k{cfg['k']}", {}).get(str(dom))
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": kern[dom]["name"], "kernel_ms": kern[dom]["ms"],
+                "algorithmic_bytes": kern[dom]["bytes"],
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback",
+                "timing": "CUDA events on the launching stream, L2 flushed before each launch, "
+                          f"mean of {args.kernel_reps} launches after the timed region",
+                "kernels": {kern[o]["name"]: {"ms": kern[o]["ms"], "GB/s": kern[o]["bytes"] / kern[o]["ms"] / 1e6,
+                                              "frac": kern[o]["bytes"] / kern[o]["ms"] / 1e6 / peak,
+                                              "launches_per_step": per_step_launches[o],
+                                              "est_share_of_step": share[o]} for o in kern}}
+
+    # ---- end to end through the public API with host buffers
+    u0_host = torch.tensor(u0_np, dtype=torch.float64).pin_memory()
+    u_host = torch.empty(n_free, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    u0_dev = torch.empty(n_free, dtype=torch.float64, device=dev)
+    u0_dev.copy_(u0_host, non_blocking=True)
+    ctx.set_state(u0_dev)
+    u_dev = ctx.vec()
+    for _ in range(args.steps):
+        ctx.advance(1)
+        ctx.get_state_into(u_dev)
+        u_host.copy_(u_dev, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": world * n_free * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": 8 * n_free / args.steps, "d2h_bytes_per_step": 8 * n_free,
+           "note": "one job through the C ABI: pinned H2D of U0, ga_set_state (initial chain, "
+                   f"{3 * cfg['k'] - 2} solves), then per step ga_advance(1) + D2H of U into pinned memory"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_name(cfg), "n_free": n_free, "dt": dt, "lambda_max": lam,
+                           "pcg_rtol": 1e-13, "pcg_iters_per_solve": its / max(1, solves),
+                           "lockstep_iters_per_step": loop_iters / steps,
+                           "l2": "flushed between timed steps (256 MiB write), working set "
+                                 f"{ctx.workspace.numel() / 2**20:.0f} MiB",
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")}}
+        if world == 1 and not args.no_cpu_baseline:
+            ref_steps = 3
+            r = oracle_timing(cfg, ref_steps, 0)
+            line["cpu_baseline"] = {"value": r["n_free"] * r["steps"] / r["seconds"], "unit": UNIT,
+                                    "cores": cpu_cores_used(), "kind": "oracle",
+                                    "sample": f"{ref_steps} steps of the same workload after {r['setup_s']:.1f}s "
+                                              "untimed oracle setup (assembly + sparse LU)",
+                                    "host_cpus": os.cpu_count()}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -104,6 +104,7 @@ typedef struct {
   int fail_block;           /* block (0-based) that failed (-1 if none)                 */
   long long kernel_launches;/* kernels of this library executed on the device since    */
                             /* the last ga_set_state (counted on the device)            */
+  long long loop_iters;     /* lock-stepped PCG iterations executed (all solves)        */
 } ga_stats;
 
 /* Generalized-alpha parameters of the k blocks (host only, no GPU).
@@ -170,6 +171,15 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream);
 /* host_map[f] = patch * (n+p)^dim + local control-point index (co-lex) of
  * free scalar DoF f, f < n_free / ncomp.  Host only. */
 ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
+
+/* Tooling: enqueue `reps` launches of one hot-path kernel with the launch
+ * configuration the step uses, on the context's scratch PCG vectors (the
+ * time-stepping state is not modified), so a caller can time it with events.
+ * op: 0 = M stencil SpMV + p.q reduction on the k lock-stepped vectors,
+ *     1 = K stencil SpMV (b = -K s), 2 = one preconditioner application
+ *     (scaling + all line sweeps + r.z/r.r reductions), 3 = predictor pass of
+ *     the stage kernel (reads the 3k chain, writes the k predictors). */
+ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream);
 
 void ga_destroy(ga_ctx* ctx);
 

@@ -41,6 +41,7 @@ struct DevStatus {
   double max_relres;
   double u0norm2;             // ||U_0||^2 for the instability detector
   unsigned long long launches;
+  long long loop_iters;       // lock-stepped PCG iterations executed
 };
 
 // Reduction scratch: partial sums per block + a completion counter per site.
@@ -109,29 +110,22 @@ __device__ __forceinline__ bool reduce_last_block(double (&v)[NV], double* parti
   __syncthreads();
   if (!last) return false;
   __threadfence();
-  // the last block sums the partials in block order, NV lanes in parallel
+  // the last block sums the partials: thread t takes a contiguous chunk of
+  // blocks, then a fixed-shape block reduction combines the chunks; the
+  // result depends only on gridDim/blockDim, not on which block finished last
   double acc[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-  // split the block range over the threads of this block, then combine in order
   const unsigned int nb = gridDim.x;
   const unsigned int chunk = (nb + blockDim.x - 1) / blockDim.x;
   unsigned int b0 = threadIdx.x * chunk, b1 = min(nb, b0 + chunk);
   for (unsigned int b = b0; b < b1; ++b)
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] += ((volatile double*)partial)[(size_t)b * NV + j];
-  // ordered combination of per-thread chunks through shared memory
-  __shared__ double shc[NTHREADS][NV > 0 ? NV : 1];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) shc[threadIdx.x][j] = acc[j];
-  __syncthreads();
+  block_sum<NV>(acc);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      double s = 0.0;
-      for (unsigned int t = 0; t < blockDim.x; ++t) s += shc[t][j];
-      out[j] = s;
-    }
+    for (int j = 0; j < NV; ++j) out[j] = acc[j];
     *counter = 0u;  // ready for the next launch
   }
   return threadIdx.x == 0;

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -35,7 +36,11 @@ struct PrecPatch {
   double* s = nullptr;  // device, box points
   double* t = nullptr;  // device, nvec*box*k (multi-patch only)
   double* L[3] = {nullptr, nullptr, nullptr};
+  double* Ff[3] = {nullptr, nullptr, nullptr};
+  double* Fb[3] = {nullptr, nullptr, nullptr};
+  int clen[3] = {0, 0, 0}, nchunk[3] = {0, 0, 0}, nlev[3] = {0, 0, 0};
   std::vector<double> hL[3], hdiag[3];
+  SweepFactor sf[3], sb[3];
 };
 
 }  // namespace
@@ -69,6 +74,7 @@ struct ga_ctx {
   cudaGraphExec_t g_step = nullptr, g_solveK = nullptr, g_solveB = nullptr;
   cudaGraph_t gr_step = nullptr, gr_solveK = nullptr, gr_solveB = nullptr;
   std::string err;
+  bool nograph = false;  // GA_NO_GRAPH=1: direct launches, host-driven PCG loop (profiling/debug)
 };
 
 namespace {
@@ -92,7 +98,7 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
   size_t off_coefM, off_coefK, off_chain, off_mv[7], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
       off_dscal;
-  std::vector<size_t> off_s, off_t, off_L[3];
+  std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
 };
 
@@ -252,6 +258,11 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
   return GA_OK;
 }
 
+size_t sweep_bytes(int n, int p) {
+  // dinv + coef + H + A (L <= 5 levels, C <= 32 chunks)
+  return align256(sizeof(double) * ((size_t)n * (1 + 2 * p) + (size_t)5 * 32 * p * p));
+}
+
 Layout make_layout(const Shape& sh) {
   Layout L;
   size_t o = 0;
@@ -266,7 +277,16 @@ Layout make_layout(const Shape& sh) {
   L.off_map = take(multi ? sizeof(long long) * sh.nfree : 0);
   L.off_pcg = take(sizeof(PcgState));
   L.off_st = take(sizeof(DevStatus));
-  const long long maxblocks = (sh.nvec * npts + NTHREADS - 1) / NTHREADS + 1;
+  // reduction partials: one slot per block of any reducing kernel; the line
+  // tile kernels can launch more blocks than the grid kernels on small grids
+  long long maxblocks = (sh.nvec * npts + NTHREADS - 1) / NTHREADS + 1;
+  for (const PrecPatch& pp : sh.prec) {
+    const long long nb0 = pp.bd[0], nb1 = pp.bd[1], nb2 = pp.bd[2];
+    const long long xt = (sh.nvec * nb1 * nb2 * sh.k + 7) / 8;            // x lines, 8 slots per tile
+    const long long yt = sh.nvec * nb2 * ((nb0 * sh.k + 7) / 8);           // y lines
+    const long long zt = sh.nvec * nb1 * ((nb0 * sh.k + 7) / 8);           // z lines
+    maxblocks = std::max(maxblocks, std::max(xt, std::max(yt, zt)) + 1);
+  }
   L.off_partial = take(sizeof(double) * 2 * KMAX * maxblocks);
   L.off_counter = take(sizeof(unsigned int) * 16);
   L.off_dscal = take(sizeof(double) * 16);
@@ -276,6 +296,7 @@ Layout make_layout(const Shape& sh) {
     L.off_s.push_back(take(sizeof(double) * nbox));
     L.off_t.push_back(take(multi ? sizeof(double) * sh.nvec * nbox * sh.k : 0));
     for (int c = 0; c < 3; ++c) L.off_L[c].push_back(take(sizeof(double) * (pp.bd[c] + sh.p + 1) * (sh.p + 1)));
+    for (int c = 0; c < 3; ++c) L.off_F[c].push_back(take(2 * sweep_bytes(pp.bd[c], sh.p)));
   }
   L.total = o;
   return L;
@@ -332,7 +353,13 @@ PrecArgs prec_args(ga_ctx* c, unsigned long long cond, int update) {
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.npatch = (int)c->prec.size();
   for (int r = 0; r < a.npatch; ++r) {
-    for (int d = 0; d < 3; ++d) { a.lo[r][d] = c->prec[r].lo[d]; a.bd[r][d] = c->prec[r].bd[d]; a.L[r][d] = c->prec[r].L[d]; }
+    for (int d = 0; d < 3; ++d) {
+      a.lo[r][d] = c->prec[r].lo[d]; a.bd[r][d] = c->prec[r].bd[d]; a.L[r][d] = c->prec[r].L[d];
+      a.Ff[r][d] = (d < c->dim) ? c->prec[r].Ff[d] : nullptr;
+      a.Fb[r][d] = (d < c->dim) ? c->prec[r].Fb[d] : nullptr;
+      a.clen[r][d] = c->prec[r].clen[d]; a.nchunk[r][d] = c->prec[r].nchunk[d]; a.nlev[r][d] = c->prec[r].nlev[d];
+      a.flen[r][d] = (int)c->prec[r].sf[d].buf.size();
+    }
     a.s[r] = c->prec[r].s;
     a.t[r] = c->prec[r].t;
   }
@@ -395,7 +422,7 @@ ga_status capture_pcg_loop(ga_ctx* ctx, cudaStream_t s) {
   size_t nd = 0;
   CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd));
   cudaGraphConditionalHandle h;
-  CK(cudaGraphConditionalHandleCreate(&h, graph, 0, 0));
+  CK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));  // 0 unless F1 runs
   launch_precond(prec_args(ctx, (unsigned long long)h, 1), s);
   CK(cudaGetLastError());
   CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd));
@@ -599,6 +626,68 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   return GA_OK;
 }
 
+// Direct execution of a graph kind (GA_NO_GRAPH): same kernels, PCG loop
+// condition evaluated on the host after a synchronisation per iteration.
+static void dbg(ga_ctx* ctx, cudaStream_t s, const char* what) {
+  static int on = -1;
+  if (on < 0) { const char* e = getenv("GA_DEBUG"); on = e && *e && *e != '0'; }
+  if (!on) return;
+  unsigned int cnt = 0;
+  PcgState h;
+  cudaMemcpyAsync(&cnt, ctx->counter, sizeof(cnt), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&h, ctx->pcg, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  fprintf(stderr, "[ga dbg] %-10s err=%d counter=%u iter=%d first=%d bb=%.3e,%.3e rr=%.3e,%.3e act=%d,%d its=%d,%d alpha=%.3e\n", what, (int)e,
+          cnt, h.iter, h.first, h.bb[0], h.bb[1], h.rr[0], h.rr[1], h.active[0], h.active[1], h.its[0], h.its[1], h.alpha[0]);
+}
+
+ga_status run_pcg_loop_direct(ga_ctx* ctx, cudaStream_t s) {
+  launch_precond(prec_args(ctx, 0ull, 1), s);
+  dbg(ctx, s, "precond0");
+  for (int guard_it = 0; guard_it < 100000; ++guard_it) {
+    PcgState h;
+    DevStatus hs;
+    CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs, ctx->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int any = 0;
+    for (int j = 0; j < ctx->k; ++j) any |= h.active[j];
+    if (!any || hs.status != 0 || h.iter >= ctx->d.pcg_maxit) break;
+    launch_p_update(vec_args(ctx), s);
+    dbg(ctx, s, "p_update");
+    launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), s);
+    dbg(ctx, s, "spmv_pq");
+    launch_precond(prec_args(ctx, 0ull, 1), s);
+    dbg(ctx, s, "precond");
+  }
+  return GA_OK;
+}
+
+ga_status run_direct(ga_ctx* ctx, GraphKind kind, cudaStream_t s) {
+  if (kind != GK_SOLVEB) launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->b, SPMV_NEGB), s);
+  dbg(ctx, s, "negb");
+  launch_init_from_b(vec_args(ctx), s);
+  dbg(ctx, s, "init_b");
+  ga_status rc = run_pcg_loop_direct(ctx, s);
+  if (rc != GA_OK) return rc;
+  if (ctx->d.pcg_refine) {
+    launch_spmv(spmv_args(ctx, 0, ctx->x, ctx->r, SPMV_TRUERES), s);
+    rc = run_pcg_loop_direct(ctx, s);
+    if (rc != GA_OK) return rc;
+  }
+  launch_solve_end(ctx->pcg, ctx->st, s);
+  if (kind == GK_STEP) launch_stage(stage_args(ctx), s);
+  CK(cudaGetLastError());
+  return GA_OK;
+}
+
+ga_status run_kind(ga_ctx* ctx, GraphKind kind, cudaStream_t s) {
+  if (ctx->nograph) return run_direct(ctx, kind, s);
+  cudaGraphExec_t e = kind == GK_STEP ? ctx->g_step : (kind == GK_SOLVEK ? ctx->g_solveK : ctx->g_solveB);
+  CK(cudaGraphLaunch(e, s));
+  return GA_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -726,6 +815,13 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       Lf.resize((size_t)(pp.bd[d] + sh.p + 1) * (sh.p + 1), 0.0);  // P zero rows for the backward sweep
       pp.hL[d] = Lf;
       pp.hdiag[d] = diag;
+      pp.sf[d] = make_sweep(Lf, pp.bd[d], sh.p, false);
+      pp.sb[d] = make_sweep(Lf, pp.bd[d], sh.p, true);
+      pp.Ff[d] = (double*)(ws + L.off_F[d][r]);
+      pp.Fb[d] = (double*)(ws + L.off_F[d][r] + sweep_bytes(pp.bd[d], sh.p));
+      pp.clen[d] = pp.sf[d].clen; pp.nchunk[d] = pp.sf[d].C; pp.nlev[d] = pp.sf[d].L;
+      CKD(cudaMemcpyAsync(pp.Ff[d], pp.sf[d].buf.data(), sizeof(double) * pp.sf[d].buf.size(), cudaMemcpyHostToDevice, s));
+      CKD(cudaMemcpyAsync(pp.Fb[d], pp.sb[d].buf.data(), sizeof(double) * pp.sb[d].buf.size(), cudaMemcpyHostToDevice, s));
       CKD(cudaMemcpyAsync(pp.L[d], pp.hL[d].data(), sizeof(double) * Lf.size(), cudaMemcpyHostToDevice, s));
       dd[d] = ctx->dscal;  // placeholder, replaced below
     }
@@ -747,9 +843,15 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   CKD(cudaMemsetAsync(ctx->q, 0, sizeof(double) * sh.nvec * sh.g.padded * sh.k, s));
   // graphs
   // graphs are captured on a private stream (the caller's may be the legacy stream)
-  rc = build_graph(ctx, ctx->cap, GK_STEP, &ctx->gr_step, &ctx->g_step);
-  if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEK, &ctx->gr_solveK, &ctx->g_solveK);
-  if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEB, &ctx->gr_solveB, &ctx->g_solveB);
+  {
+    const char* e = getenv("GA_NO_GRAPH");
+    ctx->nograph = e && *e && *e != '0';
+  }
+  if (!ctx->nograph) {
+    rc = build_graph(ctx, ctx->cap, GK_STEP, &ctx->gr_step, &ctx->g_step);
+    if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEK, &ctx->gr_solveK, &ctx->g_solveK);
+    if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEB, &ctx->gr_solveB, &ctx->g_solveB);
+  }
   if (rc != GA_OK) { ga_destroy(ctx); return rc; }
   CKD(cudaStreamSynchronize(s));
   *out = ctx;
@@ -797,7 +899,8 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
     for (int j = 0; j < batch; ++j)
       if (m0 + j <= 3 * k - 1) { src[j] = m0 + j - 2; dst[j] = m0 + j; }
     launch_pack(ctx->g, nvec, k, ctx->chain, src, ctx->pred, ctx->st, s);
-    CK(cudaGraphLaunch(ctx->g_solveK, s));
+    rc = run_kind(ctx, GK_SOLVEK, s);
+    if (rc != GA_OK) return rc;
     launch_unpack(ctx->g, nvec, k, ctx->x, dst, ctx->chain, ctx->st, s);
     CK(cudaGetLastError());
   }
@@ -809,7 +912,10 @@ ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream) {
   if (rc != GA_OK) return rc;
   if (nsteps < 0) { seterr(ctx, "nsteps < 0"); return GA_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
-  for (int i = 0; i < nsteps; ++i) CK(cudaGraphLaunch(ctx->g_step, s));
+  for (int i = 0; i < nsteps; ++i) {
+    rc = run_kind(ctx, GK_STEP, s);
+    if (rc != GA_OK) return rc;
+  }
   return GA_OK;
 }
 
@@ -867,6 +973,29 @@ ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream) {
   out->fail_step = h.fail_step;
   out->fail_block = h.fail_block;
   out->kernel_launches = (long long)h.launches;
+  out->loop_iters = h.loop_iters;
+  return GA_OK;
+}
+
+ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (op < 0 || op > 3 || reps < 0) { seterr(ctx, "bad op"); return GA_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int i = 0; i < reps; ++i) {
+    switch (op) {
+      case 0: launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), s); break;
+      case 1: launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->b, SPMV_NEGB), s); break;
+      case 2: {
+        PrecArgs a = prec_args(ctx, 0ull, 0);
+        a.maxit = 0x7fffffff;
+        launch_precond(a, s);
+        break;
+      }
+      default: launch_predict(stage_args(ctx), s); break;
+    }
+  }
+  CK(cudaGetLastError());
   return GA_OK;
 }
 
@@ -902,7 +1031,8 @@ ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters,
   const size_t mvbytes = sizeof(double) * ctx->nvec * ctx->g.padded * ctx->k;
   CK(cudaMemsetAsync(ctx->b, 0, mvbytes, s));
   launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_b, ctx->b, ctx->k, 0, ctx->st, s);
-  CK(cudaGraphLaunch(ctx->g_solveB, s));
+  rc = run_kind(ctx, GK_SOLVEB, s);
+  if (rc != GA_OK) return rc;
   launch_grid_to_api(ctx->g, ctx->nvec, ctx->nfree, ctx->map, ctx->x, ctx->k, 0, d_x, ctx->st, s);
   CK(cudaGetLastError());
   if (iters) {
@@ -937,7 +1067,8 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
     // normalise v (slot 0 of pred)
     launch_dot(g, nvec, k, ctx->pred, ctx->pred, dn, ctx->partial, ctx->counter, s);
     launch_scale(g, nvec, k, ctx->pred, dn, 1, s);
-    CK(cudaGraphLaunch(ctx->g_solveK, s));  // x = M^{-1}(-K v)
+    rc = run_kind(ctx, GK_SOLVEK, s);  // x = M^{-1}(-K v)
+    if (rc != GA_OK) return rc;
     // v <- x (slot 0)
     CK(cudaMemcpyAsync(ctx->pred, ctx->x, mvbytes, cudaMemcpyDeviceToDevice, s));
   }

@@ -1,5 +1,6 @@
 #include "host_math.h"
 
+#include <algorithm>
 #include <cmath>
 
 namespace ga {
@@ -215,6 +216,83 @@ int scheme_params(int k, double rb, double rs, int param_set,
   }
   if (theta_max) *theta_max = thmax;
   return 0;
+}
+
+}  // namespace ga
+
+namespace ga {
+
+SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backward) {
+  SweepFactor F;
+  F.n = n; F.p = p;
+  std::vector<double> dinv(n), coef((size_t)n * p, 0.0);
+  for (int i = 0; i < n; ++i) {
+    if (!backward) {
+      dinv[i] = Lr[(size_t)i * (p + 1)];
+      for (int u = 1; u <= p; ++u) coef[(size_t)i * p + u - 1] = (i - u >= 0) ? Lr[(size_t)i * (p + 1) + u] : 0.0;
+    } else {
+      // reversed index i' = i: original row io = n-1-i; z_io = (y_io - sum_u L_{io+u,io} z_{io+u}) / L_io,io
+      const int io = n - 1 - i;
+      dinv[i] = Lr[(size_t)io * (p + 1)];
+      for (int u = 1; u <= p; ++u)
+        coef[(size_t)i * p + u - 1] = (io + u < n) ? Lr[(size_t)(io + u) * (p + 1) + u] : 0.0;
+    }
+  }
+  int clen = (n + 31) / 32;
+  if (clen < p) clen = p;
+  if (clen > n) clen = n;
+  const int C = (n + clen - 1) / clen;
+  F.clen = clen; F.C = C;
+  // homogeneous responses H[i][u0-1] of chunk containing i to unit incoming state y_{a-u0}
+  std::vector<double> H((size_t)n * p, 0.0);
+  for (int w = 1; w < C; ++w) {
+    const int a = w * clen, b = std::min(n, a + clen);
+    for (int u0 = 1; u0 <= p; ++u0) {
+      std::vector<double> h(b - a + p, 0.0);  // h[k] <-> index a - p + k
+      h[p - u0] = 1.0;
+      for (int i = a; i < b; ++i) {
+        double v = 0.0;
+        for (int u = 1; u <= p; ++u) v -= coef[(size_t)i * p + u - 1] * h[i - u - (a - p)];
+        v *= dinv[i];
+        h[i - (a - p)] = v;
+        H[(size_t)i * p + u0 - 1] = v;
+      }
+    }
+  }
+  // T_w[u][u0] = H[b_w - u][u0]  (w = 0..C-2; chunk 0 has no incoming state: T_0 = 0)
+  const int E = C - 1;
+  int L = 0;
+  while ((1 << L) < E) ++L;
+  F.L = L;
+  std::vector<double> A((size_t)std::max(L, 0) * C * p * p, 0.0);
+  std::vector<double> cur((size_t)C * p * p, 0.0), nxt;
+  for (int w = 0; w < E; ++w) {
+    const int a = w * clen, b = std::min(n, a + clen);
+    for (int u = 1; u <= p; ++u)
+      for (int u0 = 1; u0 <= p; ++u0)
+        cur[((size_t)w * p + (u - 1)) * p + (u0 - 1)] = (w == 0) ? 0.0 : H[(size_t)(b - u) * p + u0 - 1];
+  }
+  for (int l = 0; l < L; ++l) {
+    const int d = 1 << l;
+    std::copy(cur.begin(), cur.end(), A.begin() + (size_t)l * C * p * p);
+    nxt = cur;
+    for (int w = d; w < E; ++w) {
+      // A_w <- A_w * A_{w-d}
+      for (int r = 0; r < p; ++r)
+        for (int c = 0; c < p; ++c) {
+          double s = 0.0;
+          for (int t = 0; t < p; ++t) s += cur[((size_t)w * p + r) * p + t] * cur[((size_t)(w - d) * p + t) * p + c];
+          nxt[((size_t)w * p + r) * p + c] = s;
+        }
+    }
+    cur.swap(nxt);
+  }
+  F.buf.reserve((size_t)n * (1 + 2 * p) + A.size());
+  F.buf.insert(F.buf.end(), dinv.begin(), dinv.end());
+  F.buf.insert(F.buf.end(), coef.begin(), coef.end());
+  F.buf.insert(F.buf.end(), H.begin(), H.end());
+  F.buf.insert(F.buf.end(), A.begin(), A.end());
+  return F;
 }
 
 }  // namespace ga

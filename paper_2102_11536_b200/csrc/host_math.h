@@ -40,3 +40,24 @@ int scheme_params(int k, double rb, double rs, int param_set,
                   double* alpha, double* beta, double* gamma, double* alpha_f, double* theta_max);
 
 }  // namespace ga
+
+namespace ga {
+
+// Chunked form of one triangular sweep y_i = (t_i - sum_{u=1..p} c_{i,u} y_{i-u}) * dinv_i
+// over a line of length n: the line is cut into C
+// chunks of length clen >= p; chunk w is solved locally from a zero incoming
+// state and corrected with the precomputed homogeneous responses H of its p
+// incoming values; the incoming states follow from an affine recurrence
+// sigma_{w+1} = T_w sigma_w + tau_w solved by a Kogge-Stone scan whose
+// (data-independent) matrix products A^(l)_w are precomputed here.
+// Device buffer layout (doubles): dinv[n] | coef[n][p] | H[n][p] | A[L][C][p][p]
+struct SweepFactor {
+  int n = 0, p = 0, clen = 0, C = 0, L = 0;
+  std::vector<double> buf;
+};
+// From the band Cholesky rows (L[i*(p+1)+0] = 1/L_ii, L[i*(p+1)+u] = L_{i,i-u}):
+// backward = false: forward sweep L y = t; true: backward sweep L^T z = y
+// written as a forward sweep on the reversed line.
+SweepFactor make_sweep(const std::vector<double>& Lrows, int n, int p, bool backward);
+
+}  // namespace ga

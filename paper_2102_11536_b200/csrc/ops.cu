@@ -13,6 +13,8 @@
 //                at once, per DoF, fused with the next step's predictors.
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "ops.cuh"
 
 namespace ga {
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(NTHREADS) k_spmv(SpmvArgs a) {
       PcgState* pc = a.pcg;
       pc->iter += 1;
       pc->pfirst = 0;
+      a.st->loop_iters += 1;
 #pragma unroll
       for (int j = 0; j < KK; ++j) {
         pc->pq[j] = tot[j];
@@ -298,12 +301,50 @@ static void line_dispatch(int p, double* t, const double* L, int len, long long 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tile line solver: a CTA stages ST line-slots x the
+// full line length in shared memory (coalesced), plus the sweep factors, then
+// solves them with the chunked recurrence: lane -> (slot, chunk), local
+// substitution from a zero state, Kogge-Stone scan of the chunk states,
+// correction with the precomputed homogeneous responses.  Forward (L) and
+// backward (L^T, as a forward sweep of the reversed line) back to back.
+// Single patch: the first direction fuses the PCG update x += alpha p,
+// r -= alpha q and the input scaling s o r; the last direction fuses the
+// output scaling, the r.z / r.r reductions and the PCG scalar step (F1).
+// ---------------------------------------------------------------------------
+struct TileLine {
+  double* t;
+  int mode;            // 0: slots contiguous at fixed element (y/z lines); 1: lines contiguous (x lines)
+  int n;               // line length
+  long long es;        // mode 0: element stride
+  int nrows, nr2, rowlen;
+  long long sA, sB;    // mode 0 row offset (r/nr2)*sA + (r%nr2)*sB; mode 1 line base likewise
+  int nlines, nl2, kk;
+  int ST;              // slots per tile (8, 16 or 32)
+  const double* Ff;
+  const double* Fb;
+  int flen;            // doubles per factor buffer
+  int clen, C, L;
+  // fusion (single patch; t is the z vector, offsets into x/r/p/q/s are the same)
+  int pro, epi, update;
+  const double* s;     // scaling per grid point
+  long long padkk;     // padded * kk (component stride of an MV)
+  double *x, *r;
+  const double *p_, *q;
+  PcgState* pcg;
+  double* partial;
+  unsigned int* counter;
+  double tol2;
+  int maxit;
+  unsigned long long cond;
+  DevStatus* st;
+};
+
 // F1: convergence test, beta, loop condition (thread 0 of the last block).
-__device__ void pcg_finalize_precond(const PrecArgs& a, const double* rz, const double* rr) {
-  PcgState* pc = a.pcg;
-  DevStatus* st = a.st;
+__device__ void pcg_finalize(PcgState* pc, DevStatus* st, int kk, int maxit, unsigned long long condh,
+                             const double* rz, const double* rr) {
   int any = 0;
-  for (int j = 0; j < a.kk; ++j) {
+  for (int j = 0; j < kk; ++j) {
     pc->rz[j] = rz[j];
     pc->rr[j] = rr[j];
     if (pc->active[j] && rr[j] <= pc->thr[j]) pc->active[j] = 0;
@@ -318,17 +359,245 @@ __device__ void pcg_finalize_precond(const PrecArgs& a, const double* rz, const 
   if (pc->first) pc->pfirst = 1;
   pc->first = 0;
   int cond = any;
-  if (any && pc->iter >= a.maxit) {
+  if (any && pc->iter >= maxit) {
     if (st->status == 0 && pc->phase == 0) {  // the refinement phase may stop at maxit
       st->status = -5;  // GA_ERR_NOCONV
       st->fail_step = st->steps;
-      for (int j = 0; j < a.kk; ++j)
+      for (int j = 0; j < kk; ++j)
         if (pc->active[j]) { st->fail_block = j; break; }
     }
     cond = 0;
   }
   if (st->status != 0) cond = 0;
-  if (a.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)a.cond, cond ? 1u : 0u);
+  if (condh) cudaGraphSetConditional((cudaGraphConditionalHandle)condh, cond ? 1u : 0u);
+}
+
+template <int P>
+__device__ __forceinline__ void tile_sweep(double* __restrict__ tile, int LD, double* __restrict__ bsc,
+                                           const double* __restrict__ F, const TileLine& a, bool rev) {
+  const int n = a.n, ST = a.ST, cpw = 32 / ST;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % ST;
+  const int ch = (threadIdx.x >> 5) * cpw + lane / ST;  // chunk of this thread
+  const double* dinv = F;
+  const double* coef = F + n;
+  const double* H = F + (size_t)n * (1 + P);
+  const double* A = F + (size_t)n * (1 + 2 * P);
+  const int lo = ch * a.clen, hi = min(n, lo + a.clen);
+  double y[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) y[u] = 0.0;
+  // phase A: local substitution of chunk ch from a zero incoming state
+  for (int i = lo; i < hi; ++i) {
+    const int pi = rev ? n - 1 - i : i;
+    double v = tile[pi * LD + sl];
+#pragma unroll
+    for (int u = P; u >= 1; --u) v = fma(-coef[i * P + u - 1], y[u - 1], v);
+    v *= dinv[i];
+#pragma unroll
+    for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+    y[0] = v;
+    tile[pi * LD + sl] = v;
+  }
+  // phase B: sigma_{w+1} = T_w sigma_w + tau_w, w = 0..C-2, Kogge-Stone over chunks
+  const int E = a.C - 1;
+  double b[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) b[u] = y[u];  // tau_w[u] = y_{hi-1-u}
+  for (int l = 0; l < a.L; ++l) {
+    const int d = 1 << l;
+    if (ch < E) {
+#pragma unroll
+      for (int u = 0; u < P; ++u) bsc[(ch * P + u) * ST + sl] = b[u];
+    }
+    __syncthreads();
+    if (ch < E && ch >= d) {
+      const double* Aw = A + ((size_t)l * a.C + ch) * P * P;
+      double bp[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) bp[u] = bsc[((ch - d) * P + u) * ST + sl];
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        double s2 = b[r];
+#pragma unroll
+        for (int c = 0; c < P; ++c) s2 = fma(Aw[r * P + c], bp[c], s2);
+        b[r] = s2;
+      }
+    }
+    __syncthreads();
+  }
+  if (ch < E) {
+#pragma unroll
+    for (int u = 0; u < P; ++u) bsc[(ch * P + u) * ST + sl] = b[u];
+  }
+  __syncthreads();
+  // phase C: y_i += sum_u H_{i,u} sigma_ch[u]
+  if (ch >= 1 && ch < a.C) {
+    double sg[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) sg[u] = bsc[((ch - 1) * P + u) * ST + sl];
+    for (int i = lo; i < hi; ++i) {
+      const int pi = rev ? n - 1 - i : i;
+      double v = tile[pi * LD + sl];
+#pragma unroll
+      for (int u = 0; u < P; ++u) v = fma(H[i * P + u], sg[u], v);
+      tile[pi * LD + sl] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// element e of this tile -> (tile column, global offset); returns false if outside
+struct TileMap {
+  int mode, n, ST, nsl, kk;
+  long long base;  // mode 0
+  long long es;
+  int l0, sig0, per, nl2;
+  long long sA, sB;
+};
+
+template <int P>
+__global__ void __launch_bounds__(1024) k_line_tile(TileLine a) {
+  const bool dead = a.st->status != 0;
+  if (dead) return;
+  count_launch(a.st);
+  extern __shared__ double smem[];
+  const int n = a.n, ST = a.ST, LD = ST + 1;
+  double* tile = smem;
+  double* bsc = tile + (size_t)n * LD;
+  double* Fs = bsc + (size_t)a.C * P * ST;
+  const int nthr = blockDim.x, tid = threadIdx.x;
+  // factors -> shared memory
+  for (int idx = tid; idx < 2 * a.flen; idx += nthr) Fs[idx] = idx < a.flen ? a.Ff[idx] : a.Fb[idx - a.flen];
+  long long base = 0;
+  int nsl = ST, l0 = 0, l1 = 0, sig0 = 0, per = 0;
+  if (a.mode == 0) {
+    const int tpr = (a.rowlen + ST - 1) / ST;
+    const int r = blockIdx.x / tpr;
+    const int f0 = (blockIdx.x % tpr) * ST;
+    base = (long long)(r / a.nr2) * a.sA + (long long)(r % a.nr2) * a.sB + f0;
+    nsl = min(ST, a.rowlen - f0);
+  } else {
+    sig0 = blockIdx.x * ST;
+    nsl = min(ST, a.nlines * a.kk - sig0);
+    l0 = sig0 / a.kk;
+    l1 = (sig0 + nsl - 1) / a.kk;
+    per = n * a.kk;
+  }
+  const int tot = a.mode == 0 ? ST * n : (l1 - l0 + 1) * per;
+  // ---- load (with the fused PCG update + input scaling)
+  for (int idx = tid; idx < tot; idx += nthr) {
+    long long g;
+    int col, i;
+    if (a.mode == 0) {
+      i = idx / ST; col = idx % ST;
+      if (col >= nsl) continue;
+      g = base + col + (long long)i * a.es;
+    } else {
+      const int ll = l0 + idx / per, e = idx % per;
+      col = ll * a.kk + e % a.kk - sig0;
+      if (col < 0 || col >= nsl) continue;
+      i = e / a.kk;
+      g = (long long)(ll / a.nl2) * a.sA + (long long)(ll % a.nl2) * a.sB + e;
+    }
+    double v;
+    if (a.pro) {
+      const int j = (int)(g % a.kk);
+      v = a.r[g];
+      if (a.update && !a.pcg->first) {
+        const double al = a.pcg->alpha[j];
+        if (al != 0.0) {
+          a.x[g] = fma(al, a.p_[g], a.x[g]);
+          v = fma(-al, a.q[g], v);
+          a.r[g] = v;
+        }
+      }
+      v *= a.s[(g % a.padkk) / a.kk];
+    } else {
+      v = a.t[g];
+    }
+    tile[i * LD + col] = v;
+  }
+  __syncthreads();
+  tile_sweep<P>(tile, LD, bsc, Fs, a, false);
+  tile_sweep<P>(tile, LD, bsc, Fs + a.flen, a, true);
+  // ---- store (with the fused output scaling and r.z / r.r partial sums)
+  double acc[2 * KMAX];
+#pragma unroll
+  for (int j = 0; j < 2 * KMAX; ++j) acc[j] = 0.0;
+  for (int idx = tid; idx < tot; idx += nthr) {
+    long long g;
+    int col, i;
+    if (a.mode == 0) {
+      i = idx / ST; col = idx % ST;
+      if (col >= nsl) continue;
+      g = base + col + (long long)i * a.es;
+    } else {
+      const int ll = l0 + idx / per, e = idx % per;
+      col = ll * a.kk + e % a.kk - sig0;
+      if (col < 0 || col >= nsl) continue;
+      i = e / a.kk;
+      g = (long long)(ll / a.nl2) * a.sA + (long long)(ll % a.nl2) * a.sB + e;
+    }
+    double v = tile[i * LD + col];
+    if (a.epi) {
+      v *= a.s[(g % a.padkk) / a.kk];
+      const double rv = a.r[g];
+      const int j = (int)(g % a.kk);
+#pragma unroll
+      for (int jj = 0; jj < KMAX; ++jj)
+        if (jj == j) { acc[jj] = fma(rv, v, acc[jj]); acc[KMAX + jj] = fma(rv, rv, acc[KMAX + jj]); }
+    }
+    a.t[g] = v;
+  }
+  if (a.epi) {
+    double out[2 * KMAX];
+    if (reduce_last_block<2 * KMAX>(acc, a.partial, a.counter, out))
+      pcg_finalize(a.pcg, a.st, a.kk, a.maxit, a.cond, out, out + KMAX);
+  }
+}
+
+static size_t tile_smem(int n, int C, int p, int ST, int flen) {
+  return sizeof(double) * ((size_t)n * (ST + 1) + (size_t)C * p * ST + 2 * (size_t)flen);
+}
+
+template <int P>
+static bool tile_launch(TileLine a, cudaStream_t s) {
+  if (a.C > 32) return false;
+  const int nsl_total = a.mode == 0 ? -1 : a.nlines * a.kk;
+  auto ntiles_for = [&](int st) -> long long {
+    return a.mode == 0 ? (long long)a.nrows * ((a.rowlen + st - 1) / st) : ((long long)nsl_total + st - 1) / st;
+  };
+  int ST = 32;
+  if (ntiles_for(32) < 296) ST = (ntiles_for(16) >= 148) ? 16 : 8;
+  a.ST = ST;
+  const size_t sm = tile_smem(a.n, a.C, P, ST, a.flen);
+  static size_t attr_max = 0, static_sm = (size_t)-1;
+  if (static_sm == (size_t)-1) {
+    cudaFuncAttributes fa;
+    static_sm = cudaFuncGetAttributes(&fa, k_line_tile<P>) == cudaSuccess ? fa.sharedSizeBytes : 16384;
+  }
+  if (sm + static_sm > 227 * 1024) return false;
+  if (sm > attr_max) {
+    if (cudaFuncSetAttribute(k_line_tile<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+      return false;
+    attr_max = sm;
+  }
+  const int cpw = 32 / ST;
+  const int nwarps = (a.C + cpw - 1) / cpw;
+  k_line_tile<P><<<(unsigned int)ntiles_for(ST), 32 * nwarps, sm, s>>>(a);
+  return true;
+}
+static bool tile_dispatch(int p, const TileLine& a, cudaStream_t s) {
+  switch (p) {
+    case 1: return tile_launch<1>(a, s);
+    case 2: return tile_launch<2>(a, s);
+    case 3: return tile_launch<3>(a, s);
+    case 4: return tile_launch<4>(a, s);
+    case 5: return tile_launch<5>(a, s);
+    case 6: return tile_launch<6>(a, s);
+    default: return tile_launch<7>(a, s);
+  }
 }
 
 // z = sum_r s_r o t_r (single patch: z *= s in place), then r.z and r.r.
@@ -381,17 +650,53 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
   if (reduce_last_block<2 * KK>(v, a.partial, a.counter, out)) {
     double rz[KMAX], rr[KMAX];
     for (int j = 0; j < KK; ++j) { rz[j] = out[j]; rr[j] = out[KK + j]; }
-    pcg_finalize_precond(a, rz, rr);
+    pcg_finalize(a.pcg, a.st, KK, a.maxit, a.cond, rz, rr);
   }
 }
 
 void launch_precond(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
+  const bool single = (a.npatch == 1 && a.t[0] == nullptr);
+  // fused path: single patch, tile solver available for every direction
+  bool fused = single;
+  for (int d = 0; d < g.dim && fused; ++d) fused = a.Ff[0][d] != nullptr && a.nchunk[0][d] <= 32;
+  if (fused) {
+    const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
+    const long long str[3] = {a.kk, (long long)g.nx * a.kk, (long long)g.nx * g.ny * a.kk};
+    const long long sc = g.padded * a.kk;
+    bool ok = true;
+    for (int d = 0; d < g.dim && ok; ++d) {
+      TileLine tl;
+      memset(&tl, 0, sizeof(tl));
+      tl.t = a.z + g.guard * a.kk; tl.n = bd[d]; tl.kk = a.kk; tl.st = a.st;
+      tl.Ff = a.Ff[0][d]; tl.Fb = a.Fb[0][d]; tl.flen = a.flen[0][d];
+      tl.clen = a.clen[0][d]; tl.C = a.nchunk[0][d]; tl.L = a.nlev[0][d];
+      if (d == 0) {
+        tl.mode = 1; tl.nlines = a.nvec * bd[1] * bd[2]; tl.nl2 = bd[1] * bd[2]; tl.sA = sc; tl.sB = str[1];
+      } else {
+        tl.mode = 0; tl.es = str[d]; tl.rowlen = bd[0] * a.kk;
+        const int other = (d == 1) ? 2 : 1;
+        const int nother = (g.dim == 3) ? bd[other] : 1;
+        tl.nrows = a.nvec * nother; tl.nr2 = nother; tl.sA = sc; tl.sB = (g.dim == 3) ? str[other] : 0;
+      }
+      // fusion: offsets into z (= t) are offsets into x, r, p, q (same MV layout)
+      const long long off = g.guard * a.kk;
+      tl.padkk = g.padded * a.kk;
+      tl.s = a.s[0];  // s index = (offset mod padkk)/kk = grid point
+      tl.x = a.x + off; tl.r = a.r + off; tl.p_ = a.p_ + off; tl.q = a.q + off;
+      tl.pcg = a.pcg; tl.partial = a.partial; tl.counter = a.counter;
+      tl.tol2 = a.tol2; tl.maxit = a.maxit; tl.cond = a.cond; tl.update = a.update;
+      tl.pro = (d == 0);
+      tl.epi = (d == g.dim - 1);
+      ok = tile_dispatch(a.p, tl, s);
+    }
+    if (ok) return;
+  }
+  // general path (multi-patch / very long lines)
   {
     const long long tot = (long long)a.nvec * g.npts * a.kk;
     k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
   }
-  const bool single = (a.npatch == 1 && a.t[0] == nullptr);
   for (int pr = 0; pr < a.npatch; ++pr) {
     double* t;
     long long str[3];
@@ -409,12 +714,30 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
       sc = nbox * a.kk;
     }
     for (int d = 0; d < g.dim; ++d) {
-      // the two other directions enumerate the lines (first one fastest)
-      int o1 = (d == 0) ? 1 : 0;
-      int o2 = (d == 2) ? 1 : 2;
-      int na = bd[o1], nb = (g.dim == 3) ? bd[o2] : 1;
-      long long sa = str[o1], sb = (g.dim == 3) ? str[o2] : 0;
-      line_dispatch(a.p, t, a.L[pr][d], bd[d], str[d], na, sa, nb, sb, a.kk, a.nvec, sc, a.st, s);
+      bool done = false;
+      if (a.Ff[pr][d]) {
+        TileLine tl;
+        memset(&tl, 0, sizeof(tl));
+        tl.t = t; tl.n = bd[d]; tl.kk = a.kk; tl.st = a.st;
+        tl.Ff = a.Ff[pr][d]; tl.Fb = a.Fb[pr][d]; tl.flen = a.flen[pr][d];
+        tl.clen = a.clen[pr][d]; tl.C = a.nchunk[pr][d]; tl.L = a.nlev[pr][d];
+        if (d == 0) {
+          tl.mode = 1; tl.nlines = a.nvec * bd[1] * bd[2]; tl.nl2 = bd[1] * bd[2]; tl.sA = sc; tl.sB = str[1];
+        } else {
+          tl.mode = 0; tl.es = str[d]; tl.rowlen = bd[0] * a.kk;
+          const int other = (d == 1) ? 2 : 1;
+          const int nother = (g.dim == 3) ? bd[other] : 1;
+          tl.nrows = a.nvec * nother; tl.nr2 = nother; tl.sA = sc; tl.sB = (g.dim == 3) ? str[other] : 0;
+        }
+        done = tile_dispatch(a.p, tl, s);
+      }
+      if (!done) {
+        int o1 = (d == 0) ? 1 : 0;
+        int o2 = (d == 2) ? 1 : 2;
+        int na = bd[o1], nb = (g.dim == 3) ? bd[o2] : 1;
+        long long sa = str[o1], sb = (g.dim == 3) ? str[o2] : 0;
+        line_dispatch(a.p, t, a.L[pr][d], bd[d], str[d], na, sa, nb, sb, a.kk, a.nvec, sc, a.st, s);
+      }
     }
   }
   const long long tot = (long long)a.nvec * g.npts;

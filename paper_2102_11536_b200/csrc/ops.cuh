@@ -38,6 +38,9 @@ struct PrecArgs {
   const double* s[MAXPATCH];      // scaling sqrt(Dh/D) on the box (0 on masked points)
   double* t[MAXPATCH];            // box work arrays [c][box][kk] (single patch: nullptr, uses z)
   const double* L[MAXPATCH][3];   // banded Cholesky factors per direction, (len+p) rows of p+1
+  const double* Ff[MAXPATCH][3];  // chunked sweep factors (host_math.h SweepFactor), forward
+  const double* Fb[MAXPATCH][3];  // and backward (reversed line)
+  int clen[MAXPATCH][3], nchunk[MAXPATCH][3], nlev[MAXPATCH][3], flen[MAXPATCH][3];
   const unsigned char* mask;      // grid mask (nullptr: all free)
   // PCG vectors (MV)
   double *x, *r, *z;

@@ -24,7 +24,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
 
 EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
-            "ga_lambda_max", "ga_free_dof_map", "ga_destroy", "ga_last_error"]
+            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_destroy", "ga_last_error"]
 
 
 class ga_patch(ctypes.Structure):
@@ -44,7 +44,7 @@ class ga_stats(ctypes.Structure):
     _fields_ = [("steps", c_longlong), ("solves", c_longlong), ("pcg_iters", c_longlong * 4),
                 ("last_iters", c_int * 4), ("max_iters", c_int), ("max_rel_residual", c_double),
                 ("status", c_int), ("fail_step", c_longlong), ("fail_block", c_int),
-                ("kernel_launches", c_longlong)]
+                ("kernel_launches", c_longlong), ("loop_iters", c_longlong)]
 
 
 class GAError(RuntimeError):
@@ -73,6 +73,7 @@ def _load():
         "ga_solve_mass": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int), c_void_p]),
         "ga_lambda_max": (c_int, [c_void_p, c_int, P, c_void_p]),
         "ga_free_dof_map": (c_int, [c_void_p, POINTER(c_longlong)]),
+        "ga_profile_op": (c_int, [c_void_p, c_int, c_int, c_void_p]),
         "ga_destroy": (None, [c_void_p]),
         "ga_last_error": (ctypes.c_char_p, [c_void_p]),
     }
@@ -181,6 +182,9 @@ class Context:
         _check(lib.ga_get_state(self.ctx, _ptr(u), _ptr(v), _ptr(a), self._s()), self.ctx)
         return u, v, a
 
+    def get_state_into(self, u=None, v=None, a=None):
+        _check(lib.ga_get_state(self.ctx, _ptr(u), _ptr(v), _ptr(a), self._s()), self.ctx)
+
     def get_chain(self, m):
         out = self.vec()
         _check(lib.ga_get_chain(self.ctx, m, _ptr(out), self._s()), self.ctx)
@@ -211,6 +215,9 @@ class Context:
         lam = c_double()
         _check(lib.ga_lambda_max(self.ctx, iters, byref(lam), self._s()), self.ctx)
         return lam.value
+
+    def profile_op(self, op, reps=1):
+        _check(lib.ga_profile_op(self.ctx, int(op), int(reps), self._s()), self.ctx)
 
     def free_dof_map(self):
         ncomp = self.desc.ncomp
