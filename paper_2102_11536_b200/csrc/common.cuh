@@ -57,6 +57,7 @@ struct GridDesc {
   long long npts;             // nx*ny*nz
   long long guard;            // guard elements before/after each vector
   long long padded;           // npts + 2*guard
+  long long cs;               // row stride of the stencil coefficient arrays (npts rounded up to 32)
 };
 
 __device__ __forceinline__ unsigned long long gtid() {

@@ -60,7 +60,7 @@ struct ga_ctx {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   double *coefM = nullptr, *coefK = nullptr, *chain = nullptr;
-  double *pred = nullptr, *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr;
+  double *pred = nullptr, *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr, *pv1 = nullptr;
   unsigned char* mask = nullptr;
   long long* map = nullptr;
   PcgState* pcg = nullptr;
@@ -96,7 +96,7 @@ void seterr(ga_ctx* ctx, const std::string& s) {
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t off_coefM, off_coefK, off_chain, off_mv[7], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
+  size_t off_coefM, off_coefK, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
       off_dscal;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
@@ -158,9 +158,10 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
   sh.g.dim = dim; sh.g.nx = G[0]; sh.g.ny = G[1]; sh.g.nz = dim == 3 ? G[2] : 1;
   sh.g.npts = (long long)sh.g.nx * sh.g.ny * sh.g.nz;
   long long guard = (long long)sh.p * (1 + sh.g.nx + (dim == 3 ? (long long)sh.g.nx * sh.g.ny : 0));
-  guard = (guard + 31) / 32 * 32;
+  guard = (guard + 32 + 31) / 32 * 32;  // + register-blocked SpMV window overhang
   sh.g.guard = guard;
   sh.g.padded = sh.g.npts + 2 * guard;
+  sh.g.cs = (sh.g.npts + 31) / 32 * 32;
   // occupancy of coarse cells
   std::map<long long, int> cellid;
   auto ckey = [&](int x, int y, int z) { return ((long long)z * 1000 + y) * 1000 + x; };
@@ -268,10 +269,10 @@ Layout make_layout(const Shape& sh) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
   const long long npts = sh.g.npts;
-  L.off_coefM = take(sizeof(double) * sh.S * npts);
-  L.off_coefK = take(sizeof(double) * sh.S * npts * (sh.nvec == 3 ? 9 : 1));
+  L.off_coefM = take(sizeof(double) * sh.S * sh.g.cs);
+  L.off_coefK = take(sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1));
   L.off_chain = take(sizeof(double) * 3 * sh.k * sh.nvec * sh.g.padded);
-  for (int i = 0; i < 7; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
+  for (int i = 0; i < 8; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
   const bool multi = sh.prec.size() > 1;
   L.off_mask = take(multi ? npts : 0);
   L.off_map = take(multi ? sizeof(long long) * sh.nfree : 0);
@@ -364,7 +365,7 @@ PrecArgs prec_args(ga_ctx* c, unsigned long long cond, int update) {
     a.t[r] = c->prec[r].t;
   }
   a.mask = c->mask;
-  a.x = c->x; a.r = c->r; a.z = c->z; a.p_ = c->pv; a.q = c->q;
+  a.x = c->x; a.r = c->r; a.z = c->z; a.p0 = c->pv; a.p1 = c->pv1; a.q = c->q;
   a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
   a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
   a.maxit = c->d.pcg_maxit;
@@ -381,6 +382,8 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
   a.mode = mode;
+  a.fuse_p = (mode == SPMV_PQ) ? 1 : 0;
+  a.z = c->z; a.p0 = c->pv; a.p1 = c->pv1;
   a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
   a.refine_rtol2 = c->d.pcg_refine_rtol > 0 ? c->d.pcg_refine_rtol * c->d.pcg_refine_rtol : 0.0;
   a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
@@ -435,8 +438,7 @@ ga_status capture_pcg_loop(ga_ctx* ctx, cudaStream_t s) {
   CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(ctx->aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_p_update(vec_args(ctx), ctx->aux);
-  launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), ctx->aux);
+  launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), ctx->aux);  // forms p = z + beta p on the fly
   launch_precond(prec_args(ctx, (unsigned long long)h, 1), ctx->aux);
   cudaGraph_t outg;
   CK(cudaStreamEndCapture(ctx->aux, &outg));
@@ -531,8 +533,8 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   double* X2 = dim == 3 ? take(sizeof(double) * W1 * W1 * m * m * maxq) : nullptr;
   if (off > scratch_bytes) { seterr(ctx, "scratch too small (slab)"); return GA_ERR_OOM; }
 
-  CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.npts, s));
-  CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.npts * (sh.nvec == 3 ? 9 : 1), s));
+  CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.cs, s));
+  CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1), s));
   // term list: (target block pointer, spec, derivative flags per direction)
   struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; };
   std::vector<Term> terms;
@@ -561,7 +563,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
           for (int e = 0; e < 3; ++e) {
             Term t;
             memset(&t, 0, sizeof(t));
-            t.coef = ctx->coefK + (size_t)(a * 3 + b) * sh.S * sh.g.npts;
+            t.coef = ctx->coefK + (size_t)(a * 3 + b) * sh.S * sh.g.cs;
             t.ts.kind = 2; t.ts.a = a; t.ts.b = b; t.ts.c = c; t.ts.e = e;
             t.ts.lam = ctx->d.lame_lambda; t.ts.mu = ctx->d.lame_mu;
             for (int d = 0; d < 3; ++d) { t.sflag[d] = (d == c); t.tflag[d] = (d == e); }
@@ -595,7 +597,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         f.W1 = W1; f.m = m; f.p = p; f.n = n; f.qoff = qa; f.r0 = r0; f.r1 = r1;
         for (int d = 0; d < 3; ++d) f.cell[d] = ctx->patches[r].cell[d];
         f.G[0] = sh.g.nx; f.G[1] = sh.g.ny; f.G[2] = sh.g.nz;
-        f.npts = sh.g.npts;
+        f.npts = sh.g.cs;  // row stride of the coefficient arrays
         f.mask = ctx->mask;
         if (dim == 3) {
           ContractDesc c2;
@@ -653,8 +655,6 @@ ga_status run_pcg_loop_direct(ga_ctx* ctx, cudaStream_t s) {
     int any = 0;
     for (int j = 0; j < ctx->k; ++j) any |= h.active[j];
     if (!any || hs.status != 0 || h.iter >= ctx->d.pcg_maxit) break;
-    launch_p_update(vec_args(ctx), s);
-    dbg(ctx, s, "p_update");
     launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), s);
     dbg(ctx, s, "spmv_pq");
     launch_precond(prec_args(ctx, 0ull, 1), s);
@@ -762,8 +762,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->coefM = (double*)(ws + L.off_coefM);
   ctx->coefK = (double*)(ws + L.off_coefK);
   ctx->chain = (double*)(ws + L.off_chain);
-  double** mv[7] = {&ctx->pred, &ctx->b, &ctx->x, &ctx->r, &ctx->z, &ctx->pv, &ctx->q};
-  for (int i = 0; i < 7; ++i) *mv[i] = (double*)(ws + L.off_mv[i]);
+  double** mv[8] = {&ctx->pred, &ctx->b, &ctx->x, &ctx->r, &ctx->z, &ctx->pv, &ctx->q, &ctx->pv1};
+  for (int i = 0; i < 8; ++i) *mv[i] = (double*)(ws + L.off_mv[i]);
   const bool multi = desc->npatch > 1;
   ctx->mask = multi ? (unsigned char*)(ws + L.off_mask) : nullptr;
   ctx->map = multi ? (long long*)(ws + L.off_map) : nullptr;
@@ -833,7 +833,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       dd[d] = tmp + o;
       o += pp.bd[d];
     }
-    const double* center = ctx->coefM + (ctx->S / 2) * sh.g.npts;
+    const double* center = ctx->coefM + (ctx->S / 2) * sh.g.cs;
     k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
                                                                  pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
                                                                  center, sh.g.nx, sh.g.ny, ctx->mask);

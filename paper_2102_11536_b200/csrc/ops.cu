@@ -22,166 +22,6 @@ namespace ga {
 #define CUDA_LAUNCH_CHECK()
 
 // ---------------------------------------------------------------------------
-// Stencil SpMV
-// ---------------------------------------------------------------------------
-template <int KK>
-__device__ __forceinline__ void load_row(const double* __restrict__ p, double (&v)[KK]) {
-  if constexpr (KK == 2) {
-    double2 t = __ldg(reinterpret_cast<const double2*>(p));
-    v[0] = t.x; v[1] = t.y;
-  } else if constexpr (KK == 4) {
-    double2 t0 = __ldg(reinterpret_cast<const double2*>(p));
-    double2 t1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
-  } else {
-#pragma unroll
-    for (int j = 0; j < KK; ++j) v[j] = __ldg(p + j);
-  }
-}
-
-template <int P, int NC, int KK, bool ELASTIC>
-__global__ void __launch_bounds__(NTHREADS) k_spmv(SpmvArgs a) {
-  if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
-  count_launch(a.st);
-  const GridDesc g = a.g;
-  const long long i = (long long)gtid();
-  const bool valid = i < g.npts;
-  constexpr int W = 2 * P + 1;
-  const int P3 = (g.dim == 3) ? P : 0;
-  const long long sy = g.nx, sz = (long long)g.nx * g.ny;
-  const long long S = (long long)W * W * (g.dim == 3 ? W : 1);
-  constexpr int NA = ELASTIC ? 3 : NC;  // output component vectors
-  double acc[NA][KK];
-#pragma unroll
-  for (int c = 0; c < NA; ++c)
-#pragma unroll
-    for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
-  if (valid) {
-    const double* __restrict__ coef = a.coef;
-    const double* __restrict__ x = a.x;
-    long long o = 0;
-    for (int o3 = -P3; o3 <= P3; ++o3) {
-      for (int o2 = -P; o2 <= P; ++o2) {
-        const long long rowbase = g.guard + i + o3 * sz + o2 * sy;
-#pragma unroll
-        for (int o1 = -P; o1 <= P; ++o1, ++o) {
-          const long long col = rowbase + o1;
-          if constexpr (!ELASTIC) {
-            const double cf = __ldg(coef + o * g.npts + i);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              double v[KK];
-              load_row<KK>(x + ((long long)c * g.padded + col) * KK, v);
-#pragma unroll
-              for (int j = 0; j < KK; ++j) acc[c][j] = fma(cf, v[j], acc[c][j]);
-            }
-          } else {
-            double v[3][KK];
-#pragma unroll
-            for (int bb = 0; bb < 3; ++bb) load_row<KK>(x + ((long long)bb * g.padded + col) * KK, v[bb]);
-#pragma unroll
-            for (int aa = 0; aa < 3; ++aa)
-#pragma unroll
-              for (int bb = 0; bb < 3; ++bb) {
-                const double cf = __ldg(coef + ((long long)(aa * 3 + bb) * S + o) * g.npts + i);
-#pragma unroll
-                for (int j = 0; j < KK; ++j) acc[aa][j] = fma(cf, v[bb][j], acc[aa][j]);
-              }
-          }
-        }
-      }
-    }
-  }
-  // epilogue
-  double dots[KK];
-#pragma unroll
-  for (int j = 0; j < KK; ++j) dots[j] = 0.0;
-  if (valid) {
-#pragma unroll
-    for (int c = 0; c < NA; ++c) {
-      const long long base = ((long long)c * g.padded + g.guard + i) * KK;
-#pragma unroll
-      for (int j = 0; j < KK; ++j) {
-        double v = acc[c][j];
-        if (a.mode == SPMV_NEGB) v = -v;
-        else if (a.mode == SPMV_TRUERES) { v = a.b[base + j] - v; dots[j] = fma(v, v, dots[j]); }
-        else if (a.mode == SPMV_PQ) dots[j] = fma(a.x[base + j], v, dots[j]);
-        a.y[base + j] = v;
-      }
-    }
-  }
-  if (a.mode == SPMV_PQ) {
-    double tot[KK];
-    if (reduce_last_block<KK>(dots, a.partial, a.counter, tot)) {
-      PcgState* pc = a.pcg;
-      pc->iter += 1;
-      pc->pfirst = 0;
-      a.st->loop_iters += 1;
-#pragma unroll
-      for (int j = 0; j < KK; ++j) {
-        pc->pq[j] = tot[j];
-        if (pc->active[j]) {
-          pc->alpha[j] = pc->rz[j] / tot[j];
-          pc->its[j] += 1;
-        } else {
-          pc->alpha[j] = 0.0;
-        }
-      }
-    }
-  } else if (a.mode == SPMV_TRUERES) {
-    double tot[KK];
-    if (reduce_last_block<KK>(dots, a.partial, a.counter, tot)) {
-      // restart of PCG from the true residual (refinement phase, R8)
-      PcgState* pc = a.pcg;
-      pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->phase = 1;
-#pragma unroll
-      for (int j = 0; j < KK; ++j) {
-        pc->alpha[j] = 0.0;
-        pc->active[j] = pc->bb[j] > 0.0 ? 1 : 0;
-        double thr = a.tol2 * pc->bb[j];
-        if (a.refine_rtol2 > 0.0) thr = fmin(thr, a.refine_rtol2 * tot[j]);
-        pc->thr[j] = thr;
-      }
-    }
-  }
-}
-
-template <int P, int NC, int KK>
-static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
-  const unsigned int nb = (unsigned int)((a.g.npts + NTHREADS - 1) / NTHREADS);
-  if (a.elastic) {
-    if constexpr (NC == 3) k_spmv<P, 3, KK, true><<<nb, NTHREADS, 0, s>>>(a);
-  } else {
-    k_spmv<P, NC, KK, false><<<nb, NTHREADS, 0, s>>>(a);
-  }
-}
-template <int P, int NC>
-static void spmv_nc(const SpmvArgs& a, cudaStream_t s) {
-  switch (a.kk) {
-    case 1: spmv_kk<P, NC, 1>(a, s); break;
-    case 2: spmv_kk<P, NC, 2>(a, s); break;
-    case 3: spmv_kk<P, NC, 3>(a, s); break;
-    default: spmv_kk<P, NC, 4>(a, s); break;
-  }
-}
-template <int P>
-static void spmv_p(const SpmvArgs& a, cudaStream_t s) {
-  if (a.nvec == 3) spmv_nc<P, 3>(a, s);
-  else spmv_nc<P, 1>(a, s);
-}
-void launch_spmv(const SpmvArgs& a, cudaStream_t s) {
-  switch (a.p) {
-    case 1: spmv_p<1>(a, s); break;
-    case 2: spmv_p<2>(a, s); break;
-    case 3: spmv_p<3>(a, s); break;
-    case 4: spmv_p<4>(a, s); break;
-    case 5: spmv_p<5>(a, s); break;
-    case 6: spmv_p<6>(a, s); break;
-    default: spmv_p<7>(a, s); break;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Preconditioner: scaling, line solves, Schwarz sum
 // ---------------------------------------------------------------------------
 // x += alpha p, r -= alpha q (when a PCG iteration precedes), then the scaled
@@ -201,8 +41,9 @@ __global__ void __launch_bounds__(NTHREADS) k_xr_prec_in(PrecArgs a) {
   double r = a.r[idx];
   if (a.update && !a.pcg->first) {
     const double al = a.pcg->alpha[j];
+    const double* pp = (a.pcg->iter & 1) ? a.p1 : a.p0;
     if (al != 0.0) {
-      a.x[idx] = fma(al, a.p_[idx], a.x[idx]);
+      a.x[idx] = fma(al, pp[idx], a.x[idx]);
       r = fma(-al, a.q[idx], r);
       a.r[idx] = r;
     }
@@ -330,7 +171,7 @@ struct TileLine {
   const double* s;     // scaling per grid point
   long long padkk;     // padded * kk (component stride of an MV)
   double *x, *r;
-  const double *p_, *q;
+  const double *p0, *p1, *q;
   PcgState* pcg;
   double* partial;
   unsigned int* counter;
@@ -456,10 +297,100 @@ struct TileMap {
   long long sA, sB;
 };
 
+__device__ __forceinline__ int div_kk(int e, int kk) {
+  return kk == 2 ? (e >> 1) : (kk == 1 ? e : (kk == 4 ? (e >> 2) : e / 3));
+}
+
+// One element of the tile: global offset g (relative to a.t), grid point gp
+// (index of the scaling s), rhs j, tile position (i, col).
+template <int P, bool LOAD>
+__device__ __forceinline__ void tile_elem(const TileLine& a, double* tile, int LD, long long g, long long gp, int j,
+                                          int i, int col, bool upd, const double* al, const double* pp,
+                                          double* acc) {
+  if (LOAD) {
+    double v;
+    if (a.pro) {
+      v = a.r[g];
+      const double sv = a.s[gp];
+      if (upd) {
+        double alj = al[0];
+#pragma unroll
+        for (int jj = 1; jj < KMAX; ++jj) alj = (j == jj) ? al[jj] : alj;
+        if (alj != 0.0) {
+          a.x[g] = fma(alj, pp[g], a.x[g]);
+          v = fma(-alj, a.q[g], v);
+          a.r[g] = v;
+        }
+      }
+      v *= sv;
+    } else {
+      v = a.t[g];
+    }
+    tile[i * LD + col] = v;
+  } else {
+    double v = tile[i * LD + col];
+    if (a.epi) {
+      v *= a.s[gp];
+      const double rv = a.r[g];
+#pragma unroll
+      for (int jj = 0; jj < KMAX; ++jj)
+        if (jj == j) { acc[jj] = fma(rv, v, acc[jj]); acc[KMAX + jj] = fma(rv, rv, acc[KMAX + jj]); }
+    }
+    a.t[g] = v;
+  }
+}
+
+template <int P, bool LOAD>
+__device__ __forceinline__ void tile_io(const TileLine& a, double* tile, int LD, bool upd, const double* al,
+                                        const double* pp, double* acc) {
+  const int n = a.n, ST = a.ST, nthr = blockDim.x, tid = threadIdx.x;
+  const int lgST = ST == 32 ? 5 : (ST == 16 ? 4 : 3);
+  if (a.mode == 0) {
+    // y/z lines: ST slots f0..f0+nsl-1 of one row, contiguous at every element i
+    const int tpr = (a.rowlen + ST - 1) / ST;
+    const int r = blockIdx.x / tpr;
+    const int f0 = (blockIdx.x - r * tpr) * ST;
+    const long long roff = (long long)(r % a.nr2) * a.sB;
+    const long long base = (long long)(r / a.nr2) * a.sA + roff + f0;
+    const long long gp0 = roff / a.kk;      // grid point of slot 0 at element 0 (component-free)
+    const long long ges = a.es / a.kk;
+    const int nsl = min(ST, a.rowlen - f0);
+#pragma unroll 4
+    for (int idx = tid; idx < (n << lgST); idx += nthr) {
+      const int i = idx >> lgST, col = idx & (ST - 1);
+      if (col >= nsl) continue;
+      const int f = f0 + col;
+      const int xo = div_kk(f, a.kk);
+      tile_elem<P, LOAD>(a, tile, LD, base + col + (long long)i * a.es, gp0 + xo + (long long)i * ges, f - xo * a.kk,
+                         i, col, upd, al, pp, acc);
+    }
+  } else {
+    // x lines: contiguous n*kk elements per line; slots (line, rhs) sig0..sig0+nsl-1
+    const int sig0 = blockIdx.x * ST;
+    const int nsl = min(ST, a.nlines * a.kk - sig0);
+    const int l0 = div_kk(sig0, a.kk), l1 = div_kk(sig0 + nsl - 1, a.kk);
+    const int per = n * a.kk;
+    for (int ll = l0; ll <= l1; ++ll) {
+      const int lq = ll / a.nl2;
+      const long long lr = (long long)(ll - lq * a.nl2) * a.sB;
+      const long long lbase = (long long)lq * a.sA + lr;
+      const long long lgp = lr / a.kk;
+      const int c0 = ll * a.kk - sig0;
+#pragma unroll 4
+      for (int e = tid; e < per; e += nthr) {
+        const int i = div_kk(e, a.kk);
+        const int j = e - i * a.kk;
+        const int col = c0 + j;
+        if (col < 0 || col >= nsl) continue;
+        tile_elem<P, LOAD>(a, tile, LD, lbase + e, lgp + i, j, i, col, upd, al, pp, acc);
+      }
+    }
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(1024) k_line_tile(TileLine a) {
-  const bool dead = a.st->status != 0;
-  if (dead) return;
+  if (a.st->status != 0) return;
   count_launch(a.st);
   extern __shared__ double smem[];
   const int n = a.n, ST = a.ST, LD = ST + 1;
@@ -469,87 +400,26 @@ __global__ void __launch_bounds__(1024) k_line_tile(TileLine a) {
   const int nthr = blockDim.x, tid = threadIdx.x;
   // factors -> shared memory
   for (int idx = tid; idx < 2 * a.flen; idx += nthr) Fs[idx] = idx < a.flen ? a.Ff[idx] : a.Fb[idx - a.flen];
-  long long base = 0;
-  int nsl = ST, l0 = 0, l1 = 0, sig0 = 0, per = 0;
-  if (a.mode == 0) {
-    const int tpr = (a.rowlen + ST - 1) / ST;
-    const int r = blockIdx.x / tpr;
-    const int f0 = (blockIdx.x % tpr) * ST;
-    base = (long long)(r / a.nr2) * a.sA + (long long)(r % a.nr2) * a.sB + f0;
-    nsl = min(ST, a.rowlen - f0);
-  } else {
-    sig0 = blockIdx.x * ST;
-    nsl = min(ST, a.nlines * a.kk - sig0);
-    l0 = sig0 / a.kk;
-    l1 = (sig0 + nsl - 1) / a.kk;
-    per = n * a.kk;
+  // PCG scalars of the fused update (read once)
+  bool upd = false;
+  double al[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) al[j] = 0.0;
+  const double* pp = a.p0;
+  if (a.pro && a.update && !a.pcg->first) {
+    upd = true;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) al[j] = j < a.kk ? a.pcg->alpha[j] : 0.0;
+    pp = (a.pcg->iter & 1) ? a.p1 : a.p0;
   }
-  const int tot = a.mode == 0 ? ST * n : (l1 - l0 + 1) * per;
-  // ---- load (with the fused PCG update + input scaling)
-  for (int idx = tid; idx < tot; idx += nthr) {
-    long long g;
-    int col, i;
-    if (a.mode == 0) {
-      i = idx / ST; col = idx % ST;
-      if (col >= nsl) continue;
-      g = base + col + (long long)i * a.es;
-    } else {
-      const int ll = l0 + idx / per, e = idx % per;
-      col = ll * a.kk + e % a.kk - sig0;
-      if (col < 0 || col >= nsl) continue;
-      i = e / a.kk;
-      g = (long long)(ll / a.nl2) * a.sA + (long long)(ll % a.nl2) * a.sB + e;
-    }
-    double v;
-    if (a.pro) {
-      const int j = (int)(g % a.kk);
-      v = a.r[g];
-      if (a.update && !a.pcg->first) {
-        const double al = a.pcg->alpha[j];
-        if (al != 0.0) {
-          a.x[g] = fma(al, a.p_[g], a.x[g]);
-          v = fma(-al, a.q[g], v);
-          a.r[g] = v;
-        }
-      }
-      v *= a.s[(g % a.padkk) / a.kk];
-    } else {
-      v = a.t[g];
-    }
-    tile[i * LD + col] = v;
-  }
-  __syncthreads();
-  tile_sweep<P>(tile, LD, bsc, Fs, a, false);
-  tile_sweep<P>(tile, LD, bsc, Fs + a.flen, a, true);
-  // ---- store (with the fused output scaling and r.z / r.r partial sums)
   double acc[2 * KMAX];
 #pragma unroll
   for (int j = 0; j < 2 * KMAX; ++j) acc[j] = 0.0;
-  for (int idx = tid; idx < tot; idx += nthr) {
-    long long g;
-    int col, i;
-    if (a.mode == 0) {
-      i = idx / ST; col = idx % ST;
-      if (col >= nsl) continue;
-      g = base + col + (long long)i * a.es;
-    } else {
-      const int ll = l0 + idx / per, e = idx % per;
-      col = ll * a.kk + e % a.kk - sig0;
-      if (col < 0 || col >= nsl) continue;
-      i = e / a.kk;
-      g = (long long)(ll / a.nl2) * a.sA + (long long)(ll % a.nl2) * a.sB + e;
-    }
-    double v = tile[i * LD + col];
-    if (a.epi) {
-      v *= a.s[(g % a.padkk) / a.kk];
-      const double rv = a.r[g];
-      const int j = (int)(g % a.kk);
-#pragma unroll
-      for (int jj = 0; jj < KMAX; ++jj)
-        if (jj == j) { acc[jj] = fma(rv, v, acc[jj]); acc[KMAX + jj] = fma(rv, rv, acc[KMAX + jj]); }
-    }
-    a.t[g] = v;
-  }
+  tile_io<P, true>(a, tile, LD, upd, al, pp, acc);
+  __syncthreads();
+  tile_sweep<P>(tile, LD, bsc, Fs, a, false);
+  tile_sweep<P>(tile, LD, bsc, Fs + a.flen, a, true);
+  tile_io<P, false>(a, tile, LD, upd, al, pp, acc);
   if (a.epi) {
     double out[2 * KMAX];
     if (reduce_last_block<2 * KMAX>(acc, a.partial, a.counter, out))
@@ -683,7 +553,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
       const long long off = g.guard * a.kk;
       tl.padkk = g.padded * a.kk;
       tl.s = a.s[0];  // s index = (offset mod padkk)/kk = grid point
-      tl.x = a.x + off; tl.r = a.r + off; tl.p_ = a.p_ + off; tl.q = a.q + off;
+      tl.x = a.x + off; tl.r = a.r + off; tl.p0 = a.p0 + off; tl.p1 = a.p1 + off; tl.q = a.q + off;
       tl.pcg = a.pcg; tl.partial = a.partial; tl.counter = a.counter;
       tl.tol2 = a.tol2; tl.maxit = a.maxit; tl.cond = a.cond; tl.update = a.update;
       tl.pro = (d == 0);

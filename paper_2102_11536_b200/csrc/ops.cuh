@@ -20,6 +20,9 @@ struct SpmvArgs {
   int p;
   int elastic;         // 1: 3x3 block stencil
   int mode;
+  int fuse_p;          // SPMV_PQ: form p = z + beta p_old on the fly (x is ignored)
+  const double* z;
+  double *p0, *p1;     // the two PCG direction buffers (parity of pcg->iter)
   double tol2, refine_rtol2;  // SPMV_TRUERES: thresholds of the refinement phase
   PcgState* pcg;
   DevStatus* st;
@@ -44,7 +47,7 @@ struct PrecArgs {
   const unsigned char* mask;      // grid mask (nullptr: all free)
   // PCG vectors (MV)
   double *x, *r, *z;
-  const double *p_, *q;
+  const double *p0, *p1, *q;  // p_new = (pcg->iter & 1) ? p1 : p0
   PcgState* pcg;
   DevStatus* st;
   double* partial;
