@@ -178,7 +178,8 @@ ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
  * op: 0 = M stencil SpMV + p.q reduction on the k lock-stepped vectors,
  *     1 = K stencil SpMV (b = -K s), 2 = one preconditioner application
  *     (scaling + all line sweeps + r.z/r.r reductions), 3 = predictor pass of
- *     the stage kernel (reads the 3k chain, writes the k predictors). */
+ *     the stage kernel (reads the 3k chain, writes the k predictors),
+ *     4 = M stencil SpMV without reduction, 5 = PCG direction update p = z + beta p. */
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream);
 
 void ga_destroy(ga_ctx* ctx);

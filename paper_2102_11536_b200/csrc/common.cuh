@@ -26,6 +26,7 @@ struct PcgState {
   int first;            // F1 has not run yet in this phase
   int nrhs;             // right-hand sides in use (<= KMAX)
   int phase;            // 0 main solve, 1 refinement restart
+  int guard;            // F1 calls in this phase (safety stop if F2 never ran)
 };
 
 // Device-resident run status and statistics.

@@ -280,7 +280,7 @@ Layout make_layout(const Shape& sh) {
   L.off_st = take(sizeof(DevStatus));
   // reduction partials: one slot per block of any reducing kernel; the line
   // tile kernels can launch more blocks than the grid kernels on small grids
-  long long maxblocks = (sh.nvec * npts + NTHREADS - 1) / NTHREADS + 1;
+  long long maxblocks = std::max((sh.nvec * npts + NTHREADS - 1) / NTHREADS, (npts + 31) / 32) + 1;  // grid kernels, SpMV (32 rows/block)
   for (const PrecPatch& pp : sh.prec) {
     const long long nb0 = pp.bd[0], nb1 = pp.bd[1], nb2 = pp.bd[2];
     const long long xt = (sh.nvec * nb1 * nb2 * sh.k + 7) / 8;            // x lines, 8 slots per tile
@@ -365,7 +365,8 @@ PrecArgs prec_args(ga_ctx* c, unsigned long long cond, int update) {
     a.t[r] = c->prec[r].t;
   }
   a.mask = c->mask;
-  a.x = c->x; a.r = c->r; a.z = c->z; a.p0 = c->pv; a.p1 = c->pv1; a.q = c->q;
+  a.x = c->x; a.r = c->r; a.z = c->z; a.q = c->q;
+  a.p0 = c->pv; a.p1 = c->pv;  // unfused direction update: p lives in pv (pv1 only for fuse_p)
   a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
   a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
   a.maxit = c->d.pcg_maxit;
@@ -382,7 +383,9 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
   a.mode = mode;
-  a.fuse_p = (mode == SPMV_PQ) ? 1 : 0;
+  // p = z + beta p as a separate elementwise pass (measured faster than forming
+  // it on the SpMV input window, which doubles the vector loads)
+  a.fuse_p = 0;
   a.z = c->z; a.p0 = c->pv; a.p1 = c->pv1;
   a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
   a.refine_rtol2 = c->d.pcg_refine_rtol > 0 ? c->d.pcg_refine_rtol * c->d.pcg_refine_rtol : 0.0;
@@ -438,7 +441,8 @@ ga_status capture_pcg_loop(ga_ctx* ctx, cudaStream_t s) {
   CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(ctx->aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), ctx->aux);  // forms p = z + beta p on the fly
+  launch_p_update(vec_args(ctx), ctx->aux);
+  launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), ctx->aux);
   launch_precond(prec_args(ctx, (unsigned long long)h, 1), ctx->aux);
   cudaGraph_t outg;
   CK(cudaStreamEndCapture(ctx->aux, &outg));
@@ -655,6 +659,7 @@ ga_status run_pcg_loop_direct(ga_ctx* ctx, cudaStream_t s) {
     int any = 0;
     for (int j = 0; j < ctx->k; ++j) any |= h.active[j];
     if (!any || hs.status != 0 || h.iter >= ctx->d.pcg_maxit) break;
+    launch_p_update(vec_args(ctx), s);
     launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), s);
     dbg(ctx, s, "spmv_pq");
     launch_precond(prec_args(ctx, 0ull, 1), s);
@@ -815,8 +820,13 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       Lf.resize((size_t)(pp.bd[d] + sh.p + 1) * (sh.p + 1), 0.0);  // P zero rows for the backward sweep
       pp.hL[d] = Lf;
       pp.hdiag[d] = diag;
-      pp.sf[d] = make_sweep(Lf, pp.bd[d], sh.p, false);
-      pp.sb[d] = make_sweep(Lf, pp.bd[d], sh.p, true);
+      // chunks per line: enough threads (slots x chunks) to fill the GPU, <= 32
+      long long slots = (long long)sh.nvec * sh.k;
+      for (int e = 0; e < sh.dim; ++e)
+        if (e != d) slots *= pp.bd[e];
+      const int ctarget = (int)std::max(2LL, std::min(32LL, (150000 + slots - 1) / slots));
+      pp.sf[d] = make_sweep(Lf, pp.bd[d], sh.p, false, ctarget);
+      pp.sb[d] = make_sweep(Lf, pp.bd[d], sh.p, true, ctarget);
       pp.Ff[d] = (double*)(ws + L.off_F[d][r]);
       pp.Fb[d] = (double*)(ws + L.off_F[d][r] + sweep_bytes(pp.bd[d], sh.p));
       pp.clen[d] = pp.sf[d].clen; pp.nchunk[d] = pp.sf[d].C; pp.nlev[d] = pp.sf[d].L;
@@ -980,7 +990,7 @@ ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream) {
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
   ga_status rc = check_ctx(ctx);
   if (rc != GA_OK) return rc;
-  if (op < 0 || op > 3 || reps < 0) { seterr(ctx, "bad op"); return GA_ERR_ARG; }
+  if (op < 0 || op > 5 || reps < 0) { seterr(ctx, "bad op"); return GA_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   for (int i = 0; i < reps; ++i) {
     switch (op) {
@@ -992,7 +1002,9 @@ ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
         launch_precond(a, s);
         break;
       }
-      default: launch_predict(stage_args(ctx), s); break;
+      case 3: launch_predict(stage_args(ctx), s); break;
+      case 4: launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_APPLY), s); break;
+      default: launch_p_update(vec_args(ctx), s); break;
     }
   }
   CK(cudaGetLastError());

@@ -222,7 +222,7 @@ int scheme_params(int k, double rb, double rs, int param_set,
 
 namespace ga {
 
-SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backward) {
+SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backward, int chunks_target) {
   SweepFactor F;
   F.n = n; F.p = p;
   std::vector<double> dinv(n), coef((size_t)n * p, 0.0);
@@ -238,7 +238,9 @@ SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backwar
         coef[(size_t)i * p + u - 1] = (io + u < n) ? Lr[(size_t)(io + u) * (p + 1) + u] : 0.0;
     }
   }
-  int clen = (n + 31) / 32;
+  if (chunks_target < 1) chunks_target = 1;
+  if (chunks_target > 32) chunks_target = 32;
+  int clen = (n + chunks_target - 1) / chunks_target;
   if (clen < p) clen = p;
   if (clen > n) clen = n;
   const int C = (n + clen - 1) / clen;

@@ -58,6 +58,6 @@ struct SweepFactor {
 // From the band Cholesky rows (L[i*(p+1)+0] = 1/L_ii, L[i*(p+1)+u] = L_{i,i-u}):
 // backward = false: forward sweep L y = t; true: backward sweep L^T z = y
 // written as a forward sweep on the reversed line.
-SweepFactor make_sweep(const std::vector<double>& Lrows, int n, int p, bool backward);
+SweepFactor make_sweep(const std::vector<double>& Lrows, int n, int p, bool backward, int chunks_target = 32);
 
 }  // namespace ga

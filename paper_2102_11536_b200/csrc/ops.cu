@@ -19,6 +19,13 @@
 
 namespace ga {
 
+// grid of a reducing grid-stride kernel: one completion atomic per block on a
+// single counter, so keep the block count bounded (148 SMs x 8 blocks)
+static unsigned int red_grid(long long n) {
+  const long long b = (n + NTHREADS - 1) / NTHREADS;
+  return (unsigned int)(b < 1184 ? (b > 0 ? b : 1) : 1184);
+}
+
 #define CUDA_LAUNCH_CHECK()
 
 // ---------------------------------------------------------------------------
@@ -200,6 +207,12 @@ __device__ void pcg_finalize(PcgState* pc, DevStatus* st, int kk, int maxit, uns
   if (pc->first) pc->pfirst = 1;
   pc->first = 0;
   int cond = any;
+  // safety: the iteration counter lives in F2; never loop more than maxit + 2 F1 calls
+  pc->guard += 1;
+  if ((long long)pc->guard > (long long)maxit + 2 && st->status == 0) {
+    st->status = -7;  // GA_ERR_CUDA: inconsistent device state
+    st->fail_step = st->steps;
+  }
   if (any && pc->iter >= maxit) {
     if (st->status == 0 && pc->phase == 0) {  // the refinement phase may stop at maxit
       st->status = -5;  // GA_ERR_NOCONV
@@ -477,11 +490,11 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
   if (!dead) count_launch(a.st);
   const GridDesc g = a.g;
   const long long tot = (long long)a.nvec * g.npts;
-  const long long e = (long long)gtid();
+  const long long estride = (long long)gridDim.x * blockDim.x;
   double v[2 * KK];
 #pragma unroll
   for (int j = 0; j < 2 * KK; ++j) v[j] = 0.0;
-  if (!dead && e < tot) {
+  if (!dead) for (long long e = (long long)gtid(); e < tot; e += estride) {
     const long long i = e % g.npts;
     const int c = (int)(e / g.npts);
     const long long base = ((long long)c * g.padded + g.guard + i) * KK;
@@ -511,8 +524,8 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
     for (int j = 0; j < KK; ++j) {
       a.z[base + j] = z[j];
       const double r = a.r[base + j];
-      v[j] = r * z[j];
-      v[KK + j] = r * r;
+      v[j] = fma(r, z[j], v[j]);
+      v[KK + j] = fma(r, r, v[KK + j]);
     }
   }
   if (dead) return;
@@ -611,7 +624,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     }
   }
   const long long tot = (long long)a.nvec * g.npts;
-  const unsigned int nb = (unsigned int)((tot + NTHREADS - 1) / NTHREADS);
+  const unsigned int nb = red_grid(tot);
   switch (a.kk) {
     case 1: k_prec_out<1><<<nb, NTHREADS, 0, s>>>(a); break;
     case 2: k_prec_out<2><<<nb, NTHREADS, 0, s>>>(a); break;
@@ -629,11 +642,11 @@ __global__ void __launch_bounds__(NTHREADS) k_init_from_b(VecArgs a) {
   if (!dead) count_launch(a.st);
   const GridDesc g = a.g;
   const long long tot = (long long)a.nvec * g.npts;
-  const long long e = (long long)gtid();
+  const long long estride = (long long)gridDim.x * blockDim.x;
   double v[KK];
 #pragma unroll
   for (int j = 0; j < KK; ++j) v[j] = 0.0;
-  if (!dead && e < tot) {
+  if (!dead) for (long long e = (long long)gtid(); e < tot; e += estride) {
     const long long i = e % g.npts;
     const int c = (int)(e / g.npts);
     const long long base = ((long long)c * g.padded + g.guard + i) * KK;
@@ -642,14 +655,14 @@ __global__ void __launch_bounds__(NTHREADS) k_init_from_b(VecArgs a) {
       const double b = a.b[base + j];
       a.r[base + j] = b;
       a.x[base + j] = 0.0;
-      v[j] = b * b;
+      v[j] = fma(b, b, v[j]);
     }
   }
   if (dead) return;
   double out[KK];
   if (reduce_last_block<KK>(v, a.partial, a.counter, out)) {
     PcgState* pc = a.pcg;
-    pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->nrhs = KK; pc->phase = 0;
+    pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->nrhs = KK; pc->phase = 0; pc->guard = 0;
     for (int j = 0; j < KK; ++j) {
       pc->bb[j] = out[j];
       pc->thr[j] = a.tol2 * out[j];
@@ -662,7 +675,7 @@ __global__ void __launch_bounds__(NTHREADS) k_init_from_b(VecArgs a) {
 }
 void launch_init_from_b(const VecArgs& a, cudaStream_t s) {
   const long long tot = (long long)a.nvec * a.g.npts;
-  const unsigned int nb = (unsigned int)((tot + NTHREADS - 1) / NTHREADS);
+  const unsigned int nb = red_grid(tot);
   switch (a.kk) {
     case 1: k_init_from_b<1><<<nb, NTHREADS, 0, s>>>(a); break;
     case 2: k_init_from_b<2><<<nb, NTHREADS, 0, s>>>(a); break;
@@ -729,9 +742,9 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
   const GridDesc g = a.g;
   const int k = a.k, n3 = 3 * a.k;
   const long long tot = (long long)a.nvec * g.npts;
-  const long long e = (long long)gtid();
+  const long long estride = (long long)gridDim.x * blockDim.x;
   double u2[1] = {0.0};
-  if (!dead && e < tot) {
+  if (!dead) for (long long e = (long long)gtid(); e < tot; e += estride) {
     const long long i = e % g.npts;
     const int c = (int)(e / g.npts);
     const long long vstride = (long long)a.nvec * g.padded;
@@ -758,7 +771,7 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
       const int d = 3 * j;
       a.pred[pb + j] = (j < k - 1) ? taylor(nw, d, n3, a.f) : nw[d];
     }
-    u2[0] = nw[0] * nw[0];
+    u2[0] = fma(nw[0], nw[0], u2[0]);
   }
   if (dead || !STEP) return;
   double out[1];
@@ -774,7 +787,7 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
 }
 void launch_stage(const StageArgs& a, cudaStream_t s) {
   const long long tot = (long long)a.nvec * a.g.npts;
-  k_stage<true><<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+  k_stage<true><<<red_grid(tot), NTHREADS, 0, s>>>(a);
 }
 void launch_predict(const StageArgs& a, cudaStream_t s) {
   const long long tot = (long long)a.nvec * a.g.npts;
@@ -868,13 +881,13 @@ void launch_grid_to_api(const GridDesc& g, int nvec, long long nfree, const long
 __global__ void __launch_bounds__(NTHREADS) k_dot(GridDesc g, int nvec, int kk, const double* a, const double* b,
                                                   double* outp, double* partial, unsigned int* counter) {
   const long long tot = (long long)nvec * g.npts;
-  const long long e = (long long)gtid();
+  const long long estride = (long long)gridDim.x * blockDim.x;
   double v[1] = {0.0};
-  if (e < tot) {
+  for (long long e = (long long)gtid(); e < tot; e += estride) {
     const long long i = e % g.npts;
     const int c = (int)(e / g.npts);
     const long long idx = ((long long)c * g.padded + g.guard + i) * kk;
-    v[0] = a[idx] * b[idx];
+    v[0] = fma(a[idx], b[idx], v[0]);
   }
   double out[1];
   if (reduce_last_block<1>(v, partial, counter, out)) *outp = out[0];
@@ -882,7 +895,7 @@ __global__ void __launch_bounds__(NTHREADS) k_dot(GridDesc g, int nvec, int kk, 
 void launch_dot(const GridDesc& g, int nvec, int kk, const double* a, const double* b, double* out, double* partial,
                 unsigned int* counter, cudaStream_t s) {
   const long long tot = (long long)nvec * g.npts;
-  k_dot<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, a, b, out, partial, counter);
+  k_dot<<<red_grid(tot), NTHREADS, 0, s>>>(g, nvec, kk, a, b, out, partial, counter);
 }
 __global__ void k_scale(GridDesc g, int nvec, int kk, double* a, const double* num, int inv_sqrt) {
   const long long tot = (long long)nvec * g.npts;

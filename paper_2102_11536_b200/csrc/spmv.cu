@@ -5,6 +5,8 @@
 // r = b - M x (refinement restart, R8).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace ga {
@@ -27,28 +29,29 @@ __device__ __forceinline__ void load_row(const double* __restrict__ p, double (&
   }
 }
 
-// Shared-memory staged stencil SpMV.  A block of
-// BR x G threads owns BR consecutive rows; thread (r, g) handles row r for the
-// offset lines (o3, o2) = g, g+G, ... .  Each chunk of G offset lines has its
-// input windows (BR + 2P points each) staged in shared memory by the group
-// that uses them (double buffered: the next chunk is prefetched into
-// registers while the current one is consumed), so every input value is read
-// from L2 once per block and line, coefficient loads are coalesced (thread =
-// row), and small grids still keep 16 warps per block in flight.  The G
-// partial sums are combined in shared memory in a fixed order.  With SPMV_PQ +
-// fuse_p the window is the new PCG direction p = z + beta p_old.
+// Warp-staged stencil SpMV.  A block of G warps
+// owns 32 consecutive rows (lane = row: coefficient loads are 256 B coalesced
+// per warp); warp w handles the offset lines (o3, o2) = w, w+G, ... .  For each
+// line the warp stages its input window (32 + 2P points) in its own slice of
+// shared memory (only __syncwarp, no block barrier inside the loop), with the
+// next line's window and coefficients prefetched into registers while the
+// current line is consumed.  The G partial sums are combined in shared memory
+// in a fixed order.  With SPMV_PQ + fuse_p the window is the new PCG direction
+// p = z + beta p_old, formed once per point and warp.
 template <int P, int NC, int KK, bool ELASTIC, int G>
-__global__ void __launch_bounds__(64 * G) k_spmv_sm(SpmvArgs a) {
+__global__ void __launch_bounds__(32 * G) k_spmv_sm(SpmvArgs a) {
   if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
   count_launch(a.st);
-  constexpr int BR = 64;
+  constexpr int BR = 32;
   constexpr int W = 2 * P + 1, WN = BR + 2 * P;
   constexpr int NA = ELASTIC ? 3 : NC, NB = ELASTIC ? 3 : NC;
+  constexpr int NCF = ELASTIC ? 9 : 1;  // coefficient arrays per offset
+  constexpr bool PCF = !ELASTIC;         // prefetch the next line's coefficients into registers
   extern __shared__ double smem_spmv[];
-  auto win = reinterpret_cast<double (*)[G][NB][WN][KK]>(smem_spmv);                        // [2][G][NB][WN][KK]
-  auto red = reinterpret_cast<double (*)[NA * KK][BR]>(smem_spmv + 2 * G * NB * WN * KK);   // [G][NA*KK][BR]
+  auto win = reinterpret_cast<double (*)[2][NB][WN][KK]>(smem_spmv);                        // [G][2][NB][WN][KK]
+  auto red = reinterpret_cast<double (*)[NA * KK][BR]>(smem_spmv + G * 2 * NB * WN * KK);   // [G][NA*KK][BR]
   const GridDesc g = a.g;
-  const int r = threadIdx.x % BR, gq = threadIdx.x / BR;
+  const int r = threadIdx.x & 31, gq = threadIdx.x >> 5;
   const long long i0 = (long long)blockIdx.x * BR;
   const long long i = i0 + r;
   const int W3 = (g.dim == 3) ? W : 1;
@@ -72,7 +75,9 @@ __global__ void __launch_bounds__(64 * G) k_spmv_sm(SpmvArgs a) {
     for (int j = 0; j < KK; ++j) beta[j] = a.pcg->beta[j];
     xin = a.z;
   }
-  auto fetch = [&](int line, int q, int c, double (&v)[KK]) {
+  const bool valid = i < g.npts;
+  const long long icl = valid ? i : (g.npts - 1);  // clamp coefficient reads of the tail rows
+  auto fetch_win = [&](int line, int q, int c, double (&v)[KK]) {
     const int o3 = line / W - P3, o2 = line % W - P;
     const long long pos = g.guard + i0 - P + q + o3 * sz + o2 * sy;
     const long long e = ((long long)c * g.padded + pos) * KK;
@@ -84,81 +89,80 @@ __global__ void __launch_bounds__(64 * G) k_spmv_sm(SpmvArgs a) {
       for (int j = 0; j < KK; ++j) v[j] = fma(beta[j], po[j], v[j]);
     }
   };
+  auto fetch_cf = [&](int line, double (&cf)[PCF ? W : 1][NCF]) {
+    if constexpr (!PCF) return;
+    const double* cb = a.coef + (long long)line * W * g.cs + icl;
+#pragma unroll
+    for (int o1 = 0; o1 < W; ++o1)
+#pragma unroll
+      for (int ab = 0; ab < NCF; ++ab) cf[o1][ab] = __ldg(cb + ((long long)ab * S + o1) * g.cs);
+  };
   const int nlines = W3 * W;
-  const int nch = (nlines + G - 1) / G;
   const bool two = r < 2 * P;
-  double pre[2][NB][KK];
-  {
-    const int line = gq;
-    if (line < nlines) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        fetch(line, r, c, pre[0][c]);
-        if (two) fetch(line, BR + r, c, pre[1][c]);
-#pragma unroll
-        for (int j = 0; j < KK; ++j) {
-          win[0][gq][c][r][j] = pre[0][c][j];
-          if (two) win[0][gq][c][BR + r][j] = pre[1][c][j];
-        }
-      }
-    }
-  }
-  __syncthreads();
   double acc[NA][KK];
 #pragma unroll
   for (int c = 0; c < NA; ++c)
 #pragma unroll
     for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
-  const bool valid = i < g.npts;
-  for (int ch = 0; ch < nch; ++ch) {
-    const int buf = ch & 1;
-    const int line = ch * G + gq;
-    const int nline = line + G;
-    const bool more = ch + 1 < nch && nline < nlines;
-    if (more) {
+  double pw[2][NB][KK];
+  double cf[PCF ? W : 1][NCF];
+  int line = gq;
+  if (line < nlines) {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      fetch_win(line, r, c, pw[0][c]);
+      if (two) fetch_win(line, BR + r, c, pw[1][c]);
+    }
+    fetch_cf(line, cf);
+  }
+  int buf = 0;
+  for (; line < nlines; line += G) {
+    // publish the prefetched window of `line`
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        win[gq][buf][c][r][j] = pw[0][c][j];
+        if (two) win[gq][buf][c][BR + r][j] = pw[1][c][j];
+      }
+    double ccur[PCF ? W : 1][NCF];
+    if constexpr (PCF) {
+#pragma unroll
+      for (int o1 = 0; o1 < W; ++o1) ccur[o1][0] = cf[o1][0];
+    }
+    const double* cbl = a.coef + (long long)line * W * g.cs + icl;
+    __syncwarp();
+    // prefetch the next line of this warp
+    const int nl = line + G;
+    if (nl < nlines) {
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        fetch(nline, r, c, pre[0][c]);
-        if (two) fetch(nline, BR + r, c, pre[1][c]);
+        fetch_win(nl, r, c, pw[0][c]);
+        if (two) fetch_win(nl, BR + r, c, pw[1][c]);
       }
+      fetch_cf(nl, cf);
     }
-    if (valid && line < nlines) {
-      const double* cb = a.coef + (long long)line * W * g.cs + i;
+#pragma unroll
+    for (int o1 = 0; o1 < W; ++o1) {
       if constexpr (!ELASTIC) {
-        double cf[W];
 #pragma unroll
-        for (int o1 = 0; o1 < W; ++o1) cf[o1] = __ldg(cb + (long long)o1 * g.cs);
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int o1 = 0; o1 < W; ++o1)
-#pragma unroll
-          for (int c = 0; c < NC; ++c)
-#pragma unroll
-            for (int j = 0; j < KK; ++j) acc[c][j] = fma(cf[o1], win[buf][gq][c][r + o1][j], acc[c][j]);
+          for (int j = 0; j < KK; ++j) acc[c][j] = fma(ccur[o1][0], win[gq][buf][c][r + o1][j], acc[c][j]);
       } else {
 #pragma unroll
-        for (int o1 = 0; o1 < W; ++o1)
+        for (int aa = 0; aa < 3; ++aa)
 #pragma unroll
-          for (int aa = 0; aa < 3; ++aa)
+          for (int bb = 0; bb < 3; ++bb) {
+            const double c9 = __ldg(cbl + ((long long)(aa * 3 + bb) * S + o1) * g.cs);
 #pragma unroll
-            for (int bb = 0; bb < 3; ++bb) {
-              const double cf = __ldg(cb + ((long long)(aa * 3 + bb) * S + o1) * g.cs);
-#pragma unroll
-              for (int j = 0; j < KK; ++j) acc[aa][j] = fma(cf, win[buf][gq][bb][r + o1][j], acc[aa][j]);
-            }
+            for (int j = 0; j < KK; ++j) acc[aa][j] = fma(c9, win[gq][buf][bb][r + o1][j], acc[aa][j]);
+          }
       }
     }
-    if (more) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-#pragma unroll
-        for (int j = 0; j < KK; ++j) {
-          win[buf ^ 1][gq][c][r][j] = pre[0][c][j];
-          if (two) win[buf ^ 1][gq][c][BR + r][j] = pre[1][c][j];
-        }
-    }
-    __syncthreads();
+    buf ^= 1;
   }
-  // combine the G groups (fixed order) and run the epilogue in group 0
+  // combine the G warps (fixed order) and run the epilogue in warp 0
 #pragma unroll
   for (int c = 0; c < NA; ++c)
 #pragma unroll
@@ -199,44 +203,65 @@ __global__ void __launch_bounds__(64 * G) k_spmv_sm(SpmvArgs a) {
       }
     }
   }
-  if (a.mode == SPMV_PQ) {
-    double tot[KK];
-    if (reduce_last_block<KK>(dots, a.partial, a.counter, tot)) {
-      PcgState* pc = a.pcg;
-      pc->iter += 1;
-      pc->pfirst = 0;
-      a.st->loop_iters += 1;
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) {
+    // per-block partial sums; the scalar step runs in k_spmv_fin (one block),
+    // which avoids a fence + same-address atomic per block
+    block_sum<KK>(dots);
+    if (threadIdx.x == 0) {
 #pragma unroll
-      for (int j = 0; j < KK; ++j) {
-        pc->pq[j] = tot[j];
-        if (pc->active[j]) {
-          pc->alpha[j] = pc->rz[j] / tot[j];
-          pc->its[j] += 1;
-        } else {
-          pc->alpha[j] = 0.0;
-        }
+      for (int j = 0; j < KK; ++j) a.partial[(size_t)blockIdx.x * KK + j] = dots[j];
+    }
+  }
+}
+
+// Fixed-order sum of the SpMV block partials and the PCG scalar step:
+// SPMV_PQ: alpha_j = r.z / p.q (F2); SPMV_TRUERES: restart of the refinement phase.
+template <int KK>
+__global__ void __launch_bounds__(1024) k_spmv_fin(SpmvArgs a, unsigned int nblocks) {
+  if (a.st->status != 0) return;
+  count_launch(a.st);
+  double acc[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) acc[j] = 0.0;
+  const unsigned int chunk = (nblocks + blockDim.x - 1) / blockDim.x;
+  const unsigned int b0 = threadIdx.x * chunk, b1 = min(nblocks, b0 + chunk);
+  for (unsigned int b = b0; b < b1; ++b)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) acc[j] += a.partial[(size_t)b * KK + j];
+  block_sum<KK>(acc);
+  if (threadIdx.x != 0) return;
+  PcgState* pc = a.pcg;
+  if (a.mode == SPMV_PQ) {
+    pc->iter += 1;
+    pc->pfirst = 0;
+    a.st->loop_iters += 1;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      pc->pq[j] = acc[j];
+      if (pc->active[j]) {
+        pc->alpha[j] = pc->rz[j] / acc[j];
+        pc->its[j] += 1;
+      } else {
+        pc->alpha[j] = 0.0;
       }
     }
-  } else if (a.mode == SPMV_TRUERES) {
-    double tot[KK];
-    if (reduce_last_block<KK>(dots, a.partial, a.counter, tot)) {
-      PcgState* pc = a.pcg;
-      pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->phase = 1;
+  } else {
+    // restart of PCG from the true residual (refinement phase, R8)
+    pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->phase = 1; pc->guard = 0;
 #pragma unroll
-      for (int j = 0; j < KK; ++j) {
-        pc->alpha[j] = 0.0;
-        pc->active[j] = pc->bb[j] > 0.0 ? 1 : 0;
-        double thr = a.tol2 * pc->bb[j];
-        if (a.refine_rtol2 > 0.0) thr = fmin(thr, a.refine_rtol2 * tot[j]);
-        pc->thr[j] = thr;
-      }
+    for (int j = 0; j < KK; ++j) {
+      pc->alpha[j] = 0.0;
+      pc->active[j] = pc->bb[j] > 0.0 ? 1 : 0;
+      double thr = a.tol2 * pc->bb[j];
+      if (a.refine_rtol2 > 0.0) thr = fmin(thr, a.refine_rtol2 * acc[j]);
+      pc->thr[j] = thr;
     }
   }
 }
 
 template <int P, int NC, int KK, bool ELASTIC, int G>
 static void launch_sm(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
-  constexpr int BR = 64, W = 2 * P + 1, WN = BR + 2 * P;
+  constexpr int BR = 32, W = 2 * P + 1, WN = BR + 2 * P;
   constexpr int NA = ELASTIC ? 3 : NC, NB = ELASTIC ? 3 : NC;
   constexpr size_t bytes = sizeof(double) * (2 * G * NB * WN * KK + G * NA * KK * BR);
   static bool attr = false;
@@ -244,17 +269,16 @@ static void launch_sm(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
     cudaFuncSetAttribute(k_spmv_sm<P, NC, KK, ELASTIC, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     attr = true;
   }
-  k_spmv_sm<P, NC, KK, ELASTIC, G><<<nb, 64 * G, bytes, s>>>(a);
+  k_spmv_sm<P, NC, KK, ELASTIC, G><<<nb, 32 * G, bytes, s>>>(a);
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) k_spmv_fin<KK><<<1, 1024, 0, s>>>(a, nb);
 }
 
 template <int P, int NC, int KK>
 static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
   {
-    const unsigned int nb = (unsigned int)((a.g.npts + 63) / 64);
+    const unsigned int nb = (unsigned int)((a.g.npts + 31) / 32);
     if (a.elastic) {
       if constexpr (NC == 3) launch_sm<P, 3, KK, true, 4>(a, nb, s);
-    } else if constexpr (NC == 3) {
-      launch_sm<P, NC, KK, false, 4>(a, nb, s);
     } else {
       launch_sm<P, NC, KK, false, 8>(a, nb, s);
     }

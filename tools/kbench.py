@@ -48,9 +48,9 @@ def timed(fn, n, cold):
     return np.median(ts)
 
 
-names = ["spmv_M(PQ,fused p)", "spmv_K", "precond", "predict"]
+names = ["spmv_M(PQ)", "spmv_K(NEGB)", "precond", "predict", "spmv_M(APPLY)", "p_update"]
 print(f"config {cfg['name']} p={cfg['p']} n={cfg['n']} k={cfg['k']} N={ctx.n_free}")
-for op in range(4):
+for op in range(6):
     warm_batch = timed(lambda: ctx.profile_op(op, reps), 3, False) / reps
     cold = timed(lambda: ctx.profile_op(op, 1), 10, True)
     print(f"  {names[op]:22s} warm(batched) {warm_batch:8.2f} us   cold {cold:8.2f} us")
