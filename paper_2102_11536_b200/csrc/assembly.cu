@@ -1,5 +1,5 @@
 // GPU assembly of M and K into the column-index-free stencil layout
-// coef[o][row] (o in [-p,p]^d, lexicographic, x fastest; row = global grid
+// coef[row/32][ab][o][row%32] (o in [-p,p]^d, lexicographic, x fastest; row = global grid
 // point), by global sum factorisation over the tensor Gauss grid.
 //
 // Definitions (weak form of P:57; elasticity DESIGN.md "Elasticity"):
@@ -217,7 +217,8 @@ __global__ void k_contract_final(const double* __restrict__ in, const double* __
   for (int q = qs; q < qe; ++q) s = fma(__ldg(Ai + (q - qs)), __ldg(src + (long long)(q - f.qoff) * sq), s);
   // stencil offset index, lexicographic with x fastest
   long long olin = (oo[0] + f.p) + (long long)W1 * ((oo[1] + f.p) + (DIM == 3 ? (long long)W1 * (oo[2] + f.p) : 0));
-  coef[olin * f.npts + grow] += s;
+  // blocked layout: 32-row slices, all NCF*S offsets of a slice contiguous
+  coef[((grow >> 5) * f.ncf * f.S + (long long)f.ab * f.S + olin) * 32 + (grow & 31)] += s;
 }
 
 static inline unsigned int nblk(long long n) { return (unsigned int)((n + 255) / 256); }

@@ -31,6 +31,8 @@ struct FinalDesc {
   int cell[3];
   int G[3];
   long long npts;
+  long long S;                 // offsets per coefficient array
+  int ncf, ab;                 // coefficient arrays per row slice (1 or 9) and the target block
   const unsigned char* mask;
 };
 

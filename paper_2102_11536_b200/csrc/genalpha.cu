@@ -320,7 +320,7 @@ size_t asm_fixed_bytes(const Shape& sh) {
 }
 
 __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, int loz, const double* d0,
-                          const double* d1, const double* d2, const double* coefM_center, int nx, int ny,
+                          const double* d1, const double* d2, const double* coefM, long long S, int nx, int ny,
                           const unsigned char* mask) {
   const long long nbox = (long long)bx * by * bz;
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -330,7 +330,7 @@ __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, i
   double v = 0.0;
   if (!mask || mask[gi]) {
     const double dh = d0[ix] * d1[iy] * (d2 ? d2[iz] : 1.0);
-    const double D = coefM_center[gi];
+    const double D = coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)];  // diag(M), blocked layout
     v = sqrt(dh / D);  // s = sqrt(Dh / D): calM^{-1} = S Mh^{-1} S
   }
   s[e] = v;
@@ -540,7 +540,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.cs, s));
   CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1), s));
   // term list: (target block pointer, spec, derivative flags per direction)
-  struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; };
+  struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; int ab; };
   std::vector<Term> terms;
   {
     Term t;
@@ -567,7 +567,8 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
           for (int e = 0; e < 3; ++e) {
             Term t;
             memset(&t, 0, sizeof(t));
-            t.coef = ctx->coefK + (size_t)(a * 3 + b) * sh.S * sh.g.cs;
+            t.coef = ctx->coefK;
+            t.ab = a * 3 + b;
             t.ts.kind = 2; t.ts.a = a; t.ts.b = b; t.ts.c = c; t.ts.e = e;
             t.ts.lam = ctx->d.lame_lambda; t.ts.mu = ctx->d.lame_mu;
             for (int d = 0; d < 3; ++d) { t.sflag[d] = (d == c); t.tflag[d] = (d == e); }
@@ -601,7 +602,10 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         f.W1 = W1; f.m = m; f.p = p; f.n = n; f.qoff = qa; f.r0 = r0; f.r1 = r1;
         for (int d = 0; d < 3; ++d) f.cell[d] = ctx->patches[r].cell[d];
         f.G[0] = sh.g.nx; f.G[1] = sh.g.ny; f.G[2] = sh.g.nz;
-        f.npts = sh.g.cs;  // row stride of the coefficient arrays
+        f.npts = sh.g.cs;
+        f.S = sh.S;
+        f.ncf = (t.coef == ctx->coefK && sh.nvec == 3) ? 9 : 1;
+        f.ab = t.ab;
         f.mask = ctx->mask;
         if (dim == 3) {
           ContractDesc c2;
@@ -843,10 +847,10 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       dd[d] = tmp + o;
       o += pp.bd[d];
     }
-    const double* center = ctx->coefM + (ctx->S / 2) * sh.g.cs;
+    const double* center = ctx->coefM;  // blocked layout: k_scaling indexes offset S/2
     k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
                                                                  pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
-                                                                 center, sh.g.nx, sh.g.ny, ctx->mask);
+                                                                 center, ctx->S, sh.g.nx, sh.g.ny, ctx->mask);
     CKD(cudaGetLastError());
     CKD(cudaStreamSynchronize(s));  // tmp reused by the next patch
   }

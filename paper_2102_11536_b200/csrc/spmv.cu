@@ -91,11 +91,12 @@ __global__ void __launch_bounds__(32 * G) k_spmv_sm(SpmvArgs a) {
   };
   auto fetch_cf = [&](int line, double (&cf)[PCF ? W : 1][NCF]) {
     if constexpr (!PCF) return;
-    const double* cb = a.coef + (long long)line * W * g.cs + icl;
+    // blocked layout: slice (row/32) holds NCF*S offsets x 32 rows contiguously
+    const double* cb = a.coef + ((icl >> 5) * NCF * S + (long long)line * W) * 32 + (icl & 31);
 #pragma unroll
     for (int o1 = 0; o1 < W; ++o1)
 #pragma unroll
-      for (int ab = 0; ab < NCF; ++ab) cf[o1][ab] = __ldg(cb + ((long long)ab * S + o1) * g.cs);
+      for (int ab = 0; ab < NCF; ++ab) cf[o1][ab] = __ldg(cb + ((long long)ab * S + o1) * 32);
   };
   const int nlines = W3 * W;
   const bool two = r < 2 * P;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(32 * G) k_spmv_sm(SpmvArgs a) {
 #pragma unroll
       for (int o1 = 0; o1 < W; ++o1) ccur[o1][0] = cf[o1][0];
     }
-    const double* cbl = a.coef + (long long)line * W * g.cs + icl;
+    const double* cbl = a.coef + ((icl >> 5) * NCF * S + (long long)line * W) * 32 + (icl & 31);
     __syncwarp();
     // prefetch the next line of this warp
     const int nl = line + G;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(32 * G) k_spmv_sm(SpmvArgs a) {
         for (int aa = 0; aa < 3; ++aa)
 #pragma unroll
           for (int bb = 0; bb < 3; ++bb) {
-            const double c9 = __ldg(cbl + ((long long)(aa * 3 + bb) * S + o1) * g.cs);
+            const double c9 = __ldg(cbl + ((long long)(aa * 3 + bb) * S + o1) * 32);
 #pragma unroll
             for (int j = 0; j < KK; ++j) acc[aa][j] = fma(c9, win[gq][buf][bb][r + o1][j], acc[aa][j]);
           }
