@@ -75,6 +75,8 @@ struct ga_ctx {
   cudaGraph_t gr_step = nullptr, gr_solveK = nullptr, gr_solveB = nullptr;
   std::string err;
   bool nograph = false;  // GA_NO_GRAPH=1: direct launches, host-driven PCG loop (profiling/debug)
+  bool persist = false;  // small single-patch scalar problems: one cooperative kernel per solve
+  long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
 };
 
 namespace {
@@ -280,7 +282,8 @@ Layout make_layout(const Shape& sh) {
   L.off_st = take(sizeof(DevStatus));
   // reduction partials: one slot per block of any reducing kernel; the line
   // tile kernels can launch more blocks than the grid kernels on small grids
-  long long maxblocks = std::max((sh.nvec * npts + NTHREADS - 1) / NTHREADS, (npts + 31) / 32) + 1;  // grid kernels, SpMV (32 rows/block)
+  // grid kernels, SpMV (32 rows/block), persistent solver (2 x 1184 blocks, double-buffered)
+  long long maxblocks = std::max(std::max((sh.nvec * npts + NTHREADS - 1) / NTHREADS, (npts + 31) / 32), 2LL * 1184) + 1;
   for (const PrecPatch& pp : sh.prec) {
     const long long nb0 = pp.bd[0], nb1 = pp.bd[1], nb2 = pp.bd[2];
     const long long xt = (sh.nvec * nb1 * nb2 * sh.k + 7) / 8;            // x lines, 8 slots per tile
@@ -419,6 +422,19 @@ StageArgs stage_args(ga_ctx* c) {
   return a;
 }
 
+PersistArgs persist_args(ga_ctx* ctx) {
+  PersistArgs A;
+  memset(&A, 0, sizeof(A));
+  A.pa = prec_args(ctx, 0ull, 1);
+  A.spq = spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ);
+  A.str = spmv_args(ctx, 0, ctx->x, ctx->r, SPMV_TRUERES);
+  A.va = vec_args(ctx);
+  A.refine = ctx->d.pcg_refine;
+  A.refine_rtol2 = ctx->d.pcg_refine_rtol > 0 ? ctx->d.pcg_refine_rtol * ctx->d.pcg_refine_rtol : 0.0;
+  A.trace = ctx->trace;
+  return A;
+}
+
 // One PCG phase loop: pre-loop preconditioner (sets the loop condition) and a
 // conditional WHILE node whose body is one PCG iteration.  `s` is capturing.
 ga_status capture_pcg_loop(ga_ctx* ctx, cudaStream_t s) {
@@ -451,6 +467,14 @@ ga_status capture_pcg_loop(ga_ctx* ctx, cudaStream_t s) {
 
 // b is in place: PCG (+ refinement restart) solve of M x = b for all k slots.
 ga_status capture_solve(ga_ctx* ctx, cudaStream_t s) {
+  if (ctx->persist) {
+    if (!launch_pcg_persist(persist_args(ctx), s)) {
+      seterr(ctx, "persistent PCG launch failed");
+      return GA_ERR_CUDA;
+    }
+    launch_solve_end(ctx->pcg, ctx->st, s);
+    return GA_OK;
+  }
   launch_init_from_b(vec_args(ctx), s);
   ga_status rc = capture_pcg_loop(ctx, s);
   if (rc != GA_OK) return rc;
@@ -675,6 +699,16 @@ ga_status run_pcg_loop_direct(ga_ctx* ctx, cudaStream_t s) {
 ga_status run_direct(ga_ctx* ctx, GraphKind kind, cudaStream_t s) {
   if (kind != GK_SOLVEB) launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->b, SPMV_NEGB), s);
   dbg(ctx, s, "negb");
+  if (ctx->persist) {
+    if (!launch_pcg_persist(persist_args(ctx), s)) {
+      seterr(ctx, "persistent PCG launch failed");
+      return GA_ERR_CUDA;
+    }
+    launch_solve_end(ctx->pcg, ctx->st, s);
+    if (kind == GK_STEP) launch_stage(stage_args(ctx), s);
+    CK(cudaGetLastError());
+    return GA_OK;
+  }
   launch_init_from_b(vec_args(ctx), s);
   dbg(ctx, s, "init_b");
   ga_status rc = run_pcg_loop_direct(ctx, s);
@@ -860,6 +894,15 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   {
     const char* e = getenv("GA_NO_GRAPH");
     ctx->nograph = e && *e && *e != '0';
+    const char* pe = getenv("GA_PERSIST");  // 0: never, 1: always when supported, unset: auto (small grids)
+    const bool small = (long long)sh.g.npts * sh.k <= 600000;
+    const bool want = pe ? (*pe != '0') : small;
+    ctx->persist = want && persist_supported(persist_args(ctx));
+    const char* te = getenv("GA_TRACE");
+    if (te && *te && *te != '0') {
+      cudaMalloc(&ctx->trace, 4096 * sizeof(long long));  // debug only
+      cudaMemset(ctx->trace, 0, 4096 * sizeof(long long));
+    }
   }
   if (!ctx->nograph) {
     rc = build_graph(ctx, ctx->cap, GK_STEP, &ctx->gr_step, &ctx->g_step);
@@ -1106,6 +1149,14 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
   return GA_OK;
 }
 
+// debug: copy the persistent-solver trace (GA_TRACE=1) to the host; returns slots copied
+int ga_debug_trace(ga_ctx* ctx, long long* host, int n) {
+  if (!ctx || !ctx->trace || !host) return 0;
+  if (n > 4096) n = 4096;
+  if (cudaMemcpy(host, ctx->trace, sizeof(long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
+
 ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map) {
   if (!ctx || !host_map) return GA_ERR_ARG;
   memcpy(host_map, ctx->hlocal.data(), sizeof(long long) * ctx->hlocal.size());
@@ -1120,6 +1171,7 @@ void ga_destroy(ga_ctx* ctx) {
   if (ctx->gr_step) cudaGraphDestroy(ctx->gr_step);
   if (ctx->gr_solveK) cudaGraphDestroy(ctx->gr_solveK);
   if (ctx->gr_solveB) cudaGraphDestroy(ctx->gr_solveB);
+  if (ctx->trace) cudaFree(ctx->trace);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->cap) cudaStreamDestroy(ctx->cap);
   delete ctx;

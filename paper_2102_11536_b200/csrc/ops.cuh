@@ -111,3 +111,25 @@ void launch_scale(const GridDesc& g, int nvec, int kk, double* a, const double* 
                   cudaStream_t s);
 
 }  // namespace ga
+
+namespace ga {
+
+// Persistent cooperative PCG solve (small single-patch scalar problems, where
+// every kernel is latency-bound): the whole lock-stepped solve of the k
+// right-hand sides in b -- main phase and refinement restart -- in ONE
+// cooperative launch, phases separated by grid-wide barriers, scalars
+// reduced redundantly (same order) by every block.  Returns false if the
+// configuration is not supported (caller uses the graph path).
+struct PersistArgs {
+  PrecArgs pa;        // preconditioner (single patch, fused tile path)
+  SpmvArgs spq;       // M p -> q (SPMV_PQ, unfused)
+  SpmvArgs str;       // b - M x -> r (SPMV_TRUERES)
+  VecArgs va;
+  int refine;
+  double refine_rtol2;
+  long long* trace;
+};
+bool persist_supported(const PersistArgs& A);
+bool launch_pcg_persist(const PersistArgs& A, cudaStream_t s);
+
+}  // namespace ga

@@ -1,0 +1,137 @@
+// Device core of the warp-staged stencil SpMV (included by spmv.cu and the
+// persistent solver in ops.cu).
+#pragma once
+#include "ops.cuh"
+
+namespace ga {
+
+template <int KK>
+__device__ __forceinline__ void load_row(const double* __restrict__ p, double (&v)[KK]) {
+  if constexpr (KK == 2) {
+    double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = t.x; v[1] = t.y;
+  } else if constexpr (KK == 4) {
+    double2 t0 = __ldg(reinterpret_cast<const double2*>(p));
+    double2 t1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < KK; ++j) v[j] = __ldg(p + j);
+  }
+}
+
+// Warp-owned row block: warp w of the block owns
+// the 32 consecutive rows rb = rbg*G + w (lane = row: 256-byte coalesced
+// coefficient loads from the 32-row slice) and walks all offset lines
+// (o3, o2); per line it stages its (32 + 2P)-point input window in its own
+// shared-memory slice (__syncwarp only) while the next line's window and
+// coefficients are prefetched into registers.  Warps are independent: no
+// block barrier, so many row blocks are in flight per SM.
+template <int P, int NC, int KK, bool ELASTIC, int G>
+__device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, double* smem_spmv, double (&dots)[KK]) {
+  constexpr int BR = 32;
+  constexpr int W = 2 * P + 1, WN = BR + 2 * P;
+  constexpr int NA = ELASTIC ? 3 : NC, NB = ELASTIC ? 3 : NC;
+  constexpr int NCF = ELASTIC ? 9 : 1;  // coefficient arrays per offset
+  auto win = reinterpret_cast<double (*)[2][NB][WN][KK]>(smem_spmv);  // [G][2][NB][WN][KK]
+  const GridDesc g = a.g;
+  const int r = threadIdx.x & 31, gq = threadIdx.x >> 5;
+  const long long rb = rbg * G + gq;
+  const long long i0 = rb * BR;
+  if (i0 >= g.npts) return;  // whole warp
+  const long long i = i0 + r;
+  const bool valid = i < g.npts;
+  const long long icl = valid ? i : (g.npts - 1);  // clamp coefficient reads of the tail rows
+  const int W3 = (g.dim == 3) ? W : 1;
+  const int P3 = (g.dim == 3) ? P : 0;
+  const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+  const long long S = (long long)W * W * W3;
+  const double* __restrict__ xin = a.x;
+  const double* __restrict__ cslice = a.coef + (icl >> 5) * NCF * S * 32 + (icl & 31);
+  auto fetch_win = [&](int line, int q, int c, double (&v)[KK]) {
+    const int o3 = line / W - P3, o2 = line % W - P;
+    const long long pos = g.guard + i0 - P + q + o3 * sz + o2 * sy;
+    load_row<KK>(xin + ((long long)c * g.padded + pos) * KK, v);
+  };
+  const int nlines = W3 * W;
+  const bool two = r < 2 * P;
+  double acc[NA][KK];
+#pragma unroll
+  for (int c = 0; c < NA; ++c)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
+  double pw[2][NB][KK];
+  double cf[ELASTIC ? 1 : W];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    fetch_win(0, r, c, pw[0][c]);
+    if (two) fetch_win(0, BR + r, c, pw[1][c]);
+  }
+  if constexpr (!ELASTIC) {
+#pragma unroll
+    for (int o1 = 0; o1 < W; ++o1) cf[o1] = __ldg(cslice + (long long)o1 * 32);
+  }
+  int buf = 0;
+  for (int line = 0; line < nlines; ++line) {
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        win[gq][buf][c][r][j] = pw[0][c][j];
+        if (two) win[gq][buf][c][BR + r][j] = pw[1][c][j];
+      }
+    double ccur[ELASTIC ? 1 : W];
+    if constexpr (!ELASTIC) {
+#pragma unroll
+      for (int o1 = 0; o1 < W; ++o1) ccur[o1] = cf[o1];
+    }
+    __syncwarp();
+    if (line + 1 < nlines) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        fetch_win(line + 1, r, c, pw[0][c]);
+        if (two) fetch_win(line + 1, BR + r, c, pw[1][c]);
+      }
+      if constexpr (!ELASTIC) {
+#pragma unroll
+        for (int o1 = 0; o1 < W; ++o1) cf[o1] = __ldg(cslice + ((long long)(line + 1) * W + o1) * 32);
+      }
+    }
+#pragma unroll
+    for (int o1 = 0; o1 < W; ++o1) {
+      if constexpr (!ELASTIC) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int j = 0; j < KK; ++j) acc[c][j] = fma(ccur[o1], win[gq][buf][c][r + o1][j], acc[c][j]);
+      } else {
+#pragma unroll
+        for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb) {
+            const double c9 = __ldg(cslice + ((long long)(aa * 3 + bb) * S + (long long)line * W + o1) * 32);
+#pragma unroll
+            for (int j = 0; j < KK; ++j) acc[aa][j] = fma(c9, win[gq][buf][bb][r + o1][j], acc[aa][j]);
+          }
+      }
+    }
+    buf ^= 1;
+  }
+  if (!valid) return;
+#pragma unroll
+  for (int c = 0; c < NA; ++c) {
+    const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+    double pv[KK];
+    if (a.mode == SPMV_PQ) load_row<KK>(a.x + base, pv);
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      double v = acc[c][j];
+      if (a.mode == SPMV_NEGB) v = -v;
+      else if (a.mode == SPMV_TRUERES) { v = a.b[base + j] - v; dots[j] = fma(v, v, dots[j]); }
+      else if (a.mode == SPMV_PQ) dots[j] = fma(pv[j], v, dots[j]);
+      a.y[base + j] = v;
+    }
+  }
+}
+
+}  // namespace ga
