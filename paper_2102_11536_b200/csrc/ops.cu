@@ -157,7 +157,7 @@ static void line_dispatch(int p, double* t, const double* L, int len, long long 
 namespace ga {
 
 template <int P>
-__global__ void __launch_bounds__(1024) k_line_tile(TileLine a) {
+__global__ void __launch_bounds__(512) k_line_tile(TileLine a) {
   if (a.st->status != 0) return;
   count_launch(a.st);
   extern __shared__ double smem[];
@@ -203,6 +203,8 @@ static bool tile_launch(TileLine a, cudaStream_t s) {
   };
   int ST = 32;
   if (ntiles_for(32) < 296) ST = (ntiles_for(16) >= 148) ? 16 : 8;
+  // at most 16 warps per block (launch bounds 512 -> 128 registers, no spills)
+  while (ST > 8 && (a.C + 32 / ST - 1) / (32 / ST) > 16) ST >>= 1;
   a.ST = ST;
   const size_t sm = tile_smem(a.n, a.C, P, ST, a.flen);
   static size_t attr_max = 0, static_sm = (size_t)-1;

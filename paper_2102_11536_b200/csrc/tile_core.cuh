@@ -175,86 +175,125 @@ __device__ __forceinline__ int div_kk(int e, int kk) {
 
 // One element of the tile: global offset g (relative to a.t), grid point gp
 // (index of the scaling s), rhs j, tile position (i, col).
-template <int P, bool LOAD>
-__device__ __forceinline__ void tile_elem(const TileLine& a, double* tile, int LD, long long g, long long gp, int j,
-                                          int i, int col, bool upd, const double* al, const double* pp,
-                                          double* acc) {
-  if (LOAD) {
-    double v;
-    if (a.pro) {
-      v = a.r[g];
-      const double sv = a.s[gp];
-      if (upd) {
-        double alj = al[0];
-#pragma unroll
-        for (int jj = 1; jj < KMAX; ++jj) alj = (j == jj) ? al[jj] : alj;
-        if (alj != 0.0) {
-          a.x[g] = fma(alj, pp[g], a.x[g]);
-          v = fma(-alj, a.q[g], v);
-          a.r[g] = v;
-        }
-      }
-      v *= sv;
-    } else {
-      v = a.t[g];
-    }
-    tile[i * LD + col] = v;
-  } else {
-    double v = tile[i * LD + col];
-    if (a.epi) {
-      v *= a.s[gp];
-      const double rv = a.r[g];
-#pragma unroll
-      for (int jj = 0; jj < KMAX; ++jj)
-        if (jj == j) { acc[jj] = fma(rv, v, acc[jj]); acc[KMAX + jj] = fma(rv, rv, acc[KMAX + jj]); }
-    }
-    a.t[g] = v;
-  }
-}
-
+// Tile load/store.  Each thread handles the elements idx = tid + u*nthr in
+// batches of TB: the addresses of a batch are computed first, then all its
+// global loads are issued before any is consumed (one memory round trip per
+// batch instead of one per element).
 template <int P, bool LOAD>
 __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* tile, int LD, bool upd, const double* al,
                                         const double* pp, double* acc) {
+  constexpr int TB = 4;
   const int n = a.n, ST = a.ST, nthr = blockDim.x, tid = threadIdx.x;
   const int lgST = ST == 32 ? 5 : (ST == 16 ? 4 : 3);
+  // tile geometry
+  long long base = 0, gp0 = 0, ges = 0;
+  int f0 = 0, nsl, sig0 = 0, l0 = 0, per = 1, tot;
   if (a.mode == 0) {
-    // y/z lines: ST slots f0..f0+nsl-1 of one row, contiguous at every element i
     const int tpr = (a.rowlen + ST - 1) / ST;
     const int r = tileid / tpr;
-    const int f0 = (tileid - r * tpr) * ST;
+    f0 = (tileid - r * tpr) * ST;
     const long long roff = (long long)(r % a.nr2) * a.sB;
-    const long long base = (long long)(r / a.nr2) * a.sA + roff + f0;
-    const long long gp0 = roff / a.kk;      // grid point of slot 0 at element 0 (component-free)
-    const long long ges = a.es / a.kk;
-    const int nsl = min(ST, a.rowlen - f0);
-#pragma unroll 4
-    for (int idx = tid; idx < (n << lgST); idx += nthr) {
-      const int i = idx >> lgST, col = idx & (ST - 1);
-      if (col >= nsl) continue;
-      const int f = f0 + col;
-      const int xo = div_kk(f, a.kk);
-      tile_elem<P, LOAD>(a, tile, LD, base + col + (long long)i * a.es, gp0 + xo + (long long)i * ges, f - xo * a.kk,
-                         i, col, upd, al, pp, acc);
-    }
+    base = (long long)(r / a.nr2) * a.sA + roff + f0;
+    gp0 = roff / a.kk;
+    ges = a.es / a.kk;
+    nsl = min(ST, a.rowlen - f0);
+    tot = n << lgST;
   } else {
-    // x lines: contiguous n*kk elements per line; slots (line, rhs) sig0..sig0+nsl-1
-    const int sig0 = tileid * ST;
-    const int nsl = min(ST, a.nlines * a.kk - sig0);
-    const int l0 = div_kk(sig0, a.kk), l1 = div_kk(sig0 + nsl - 1, a.kk);
-    const int per = n * a.kk;
-    for (int ll = l0; ll <= l1; ++ll) {
-      const int lq = ll / a.nl2;
-      const long long lr = (long long)(ll - lq * a.nl2) * a.sB;
-      const long long lbase = (long long)lq * a.sA + lr;
-      const long long lgp = lr / a.kk;
-      const int c0 = ll * a.kk - sig0;
-#pragma unroll 4
-      for (int e = tid; e < per; e += nthr) {
+    sig0 = tileid * ST;
+    nsl = min(ST, a.nlines * a.kk - sig0);
+    l0 = div_kk(sig0, a.kk);
+    const int l1 = div_kk(sig0 + nsl - 1, a.kk);
+    per = n * a.kk;
+    tot = (l1 - l0 + 1) * per;
+  }
+  for (int b0 = tid; b0 < tot; b0 += TB * nthr) {
+    long long g[TB], gp[TB];
+    int jj[TB], ii[TB], col[TB];
+    bool ok[TB];
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const int idx = b0 + u * nthr;
+      ok[u] = idx < tot;
+      if (a.mode == 0) {
+        const int i = idx >> lgST, c = idx & (ST - 1);
+        ok[u] = ok[u] && c < nsl;
+        const int f = f0 + c;
+        const int xo = div_kk(f, a.kk);
+        jj[u] = f - xo * a.kk;
+        ii[u] = i;
+        col[u] = c;
+        g[u] = base + c + (long long)i * a.es;
+        gp[u] = gp0 + xo + (long long)i * ges;
+      } else {
+        const int lrel = idx / per;
+        const int e = idx - lrel * per;
+        const int ll = l0 + lrel;
         const int i = div_kk(e, a.kk);
         const int j = e - i * a.kk;
-        const int col = c0 + j;
-        if (col < 0 || col >= nsl) continue;
-        tile_elem<P, LOAD>(a, tile, LD, lbase + e, lgp + i, j, i, col, upd, al, pp, acc);
+        const int c = ll * a.kk + j - sig0;
+        ok[u] = ok[u] && c >= 0 && c < nsl;
+        const int lq = ll / a.nl2;
+        const long long lr = (long long)(ll - lq * a.nl2) * a.sB;
+        jj[u] = j;
+        ii[u] = i;
+        col[u] = c;
+        g[u] = (long long)lq * a.sA + lr + e;
+        gp[u] = lr / a.kk + i;
+      }
+    }
+    if (LOAD) {
+      double v[TB], sv[TB], xv[TB], pv[TB], qv[TB];
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const long long gg = ok[u] ? g[u] : 0, gpp = ok[u] ? gp[u] : 0;
+        if (a.pro) {
+          v[u] = a.r[gg];
+          sv[u] = a.s[gpp];
+          if (upd) { xv[u] = a.x[gg]; pv[u] = pp[gg]; qv[u] = a.q[gg]; }
+        } else {
+          v[u] = a.t[gg];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        if (!ok[u]) continue;
+        double w = v[u];
+        if (a.pro) {
+          if (upd) {
+            double alj = al[0];
+#pragma unroll
+            for (int q = 1; q < KMAX; ++q) alj = (jj[u] == q) ? al[q] : alj;
+            if (alj != 0.0) {
+              a.x[g[u]] = fma(alj, pv[u], xv[u]);
+              w = fma(-alj, qv[u], w);
+              a.r[g[u]] = w;
+            }
+          }
+          w *= sv[u];
+        }
+        tile[ii[u] * LD + col[u]] = w;
+      }
+    } else {
+      double sv[TB], rv[TB];
+      if (a.epi) {
+#pragma unroll
+        for (int u = 0; u < TB; ++u) {
+          const long long gg = ok[u] ? g[u] : 0, gpp = ok[u] ? gp[u] : 0;
+          sv[u] = a.s[gpp];
+          rv[u] = a.r[gg];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        if (!ok[u]) continue;
+        double w = tile[ii[u] * LD + col[u]];
+        if (a.epi) {
+          w *= sv[u];
+#pragma unroll
+          for (int q = 0; q < KMAX; ++q)
+            if (q == jj[u]) { acc[q] = fma(rv[u], w, acc[q]); acc[KMAX + q] = fma(rv[u], rv[u], acc[KMAX + q]); }
+        }
+        a.t[g[u]] = w;
       }
     }
   }
