@@ -179,7 +179,12 @@ ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
  *     1 = K stencil SpMV (b = -K s), 2 = one preconditioner application
  *     (scaling + all line sweeps + r.z/r.r reductions), 3 = predictor pass of
  *     the stage kernel (reads the 3k chain, writes the k predictors),
- *     4 = M stencil SpMV without reduction, 5 = PCG direction update p = z + beta p. */
+ *     4 = M stencil SpMV without reduction, 5 = PCG direction update p = z + beta p,
+ *     6 = one complete lock-stepped mass solve of the current right-hand sides
+ *     (the persistent solver kernel on small grids; its step graph otherwise). */
+/* Persistent-solver mode: 1 if ga_create chose the single-kernel cooperative PCG
+ * solve (small single-patch scalar problems; env GA_PERSIST=0/1 overrides). */
+int ga_uses_persistent_solver(const ga_ctx* ctx);
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream);
 
 void ga_destroy(ga_ctx* ctx);

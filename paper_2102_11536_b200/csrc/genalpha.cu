@@ -1037,7 +1037,16 @@ ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream) {
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
   ga_status rc = check_ctx(ctx);
   if (rc != GA_OK) return rc;
-  if (op < 0 || op > 5 || reps < 0) { seterr(ctx, "bad op"); return GA_ERR_ARG; }
+  if (op < 0 || op > 6 || reps < 0) { seterr(ctx, "bad op"); return GA_ERR_ARG; }
+  if (op == 6) {
+    cudaStream_t s = (cudaStream_t)stream;
+    // one complete mass solve on the current b (persistent kernel or graph), e.g. to time it
+    for (int i = 0; i < reps; ++i) {
+      rc = run_kind(ctx, GK_SOLVEB, s);
+      if (rc != GA_OK) return rc;
+    }
+    return GA_OK;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   for (int i = 0; i < reps; ++i) {
     switch (op) {
@@ -1148,6 +1157,8 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
   if (hs.status != 0) return (ga_status)hs.status;
   return GA_OK;
 }
+
+int ga_uses_persistent_solver(const ga_ctx* ctx) { return ctx && ctx->persist ? 1 : 0; }
 
 // debug: copy the persistent-solver trace (GA_TRACE=1) to the host; returns slots copied
 int ga_debug_trace(ga_ctx* ctx, long long* host, int n) {

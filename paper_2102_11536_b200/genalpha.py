@@ -24,7 +24,8 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
 
 EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
-            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_destroy", "ga_last_error"]
+            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_destroy",
+            "ga_last_error"]
 
 
 class ga_patch(ctypes.Structure):
@@ -74,6 +75,7 @@ def _load():
         "ga_lambda_max": (c_int, [c_void_p, c_int, P, c_void_p]),
         "ga_free_dof_map": (c_int, [c_void_p, POINTER(c_longlong)]),
         "ga_profile_op": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+        "ga_uses_persistent_solver": (c_int, [c_void_p]),
         "ga_destroy": (None, [c_void_p]),
         "ga_last_error": (ctypes.c_char_p, [c_void_p]),
     }
@@ -218,6 +220,9 @@ class Context:
 
     def profile_op(self, op, reps=1):
         _check(lib.ga_profile_op(self.ctx, int(op), int(reps), self._s()), self.ctx)
+
+    def persistent(self):
+        return bool(lib.ga_uses_persistent_solver(self.ctx))
 
     def free_dof_map(self):
         ncomp = self.desc.ncomp

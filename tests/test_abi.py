@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_functions():
     src = open(os.path.join(ROOT, "include", "genalpha.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:ga_status|void|const char\*)\s+(ga_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:ga_status|void|int|const char\*)\s+(ga_\w+)\s*\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")
