@@ -895,7 +895,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     const char* e = getenv("GA_NO_GRAPH");
     ctx->nograph = e && *e && *e != '0';
     const char* pe = getenv("GA_PERSIST");  // 0: never, 1: always when supported, unset: auto (small grids)
-    const bool small = (long long)sh.g.npts * sh.k <= 600000;
+    // latency-bound regime: little data per PCG phase (C2-like); bandwidth-bound grids keep the graph path
+    const bool small = (long long)sh.g.npts * sh.k <= 600000 && (double)sh.S * sh.g.npts * 8.0 <= 64e6;
     const bool want = pe ? (*pe != '0') : small;
     ctx->persist = want && persist_supported(persist_args(ctx));
     const char* te = getenv("GA_TRACE");

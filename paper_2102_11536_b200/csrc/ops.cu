@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ops.cuh"
@@ -83,11 +84,16 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_gather(PrecArgs a, int pr) {
 }
 
 // Forward then backward substitution with the banded Cholesky factor along
-// lines of length len (element stride es); one thread per (comp, line, rhs).
+// lines of length len (element stride es); one thread per (comp, line, rhs),
+// consecutive threads = consecutive (x, rhs) so y/z lines are coalesced.
+// Streaming version for many lines (3D): the loads of the next D elements are
+// issued before the D recurrence steps of the current block (software
+// pipelining, D independent loads in flight per thread).
 template <int P>
 __global__ void __launch_bounds__(NTHREADS) k_line(double* __restrict__ t, const double* __restrict__ L, int len,
                                                    long long es, int na, long long sa, int nb, long long sb, int kk,
                                                    int nvec, long long sc, DevStatus* st) {
+  constexpr int D = 8;
   if (st->status != 0) return;
   count_launch(st);
   const long long nl = (long long)nvec * nb * na * kk;
@@ -103,30 +109,57 @@ __global__ void __launch_bounds__(NTHREADS) k_line(double* __restrict__ t, const
   double y[P];
 #pragma unroll
   for (int u = 0; u < P; ++u) y[u] = 0.0;
+  double nxt[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) nxt[d] = d < len ? base[(long long)d * es] : 0.0;
   // forward: y_i = (t_i - sum_{u=1..P} L_{i,i-u} y_{i-u}) / L_ii
-  for (int i = 0; i < len; ++i) {
-    double v = base[(long long)i * es];
-    const double* Li = L + (long long)i * (P + 1);
+  for (int i0 = 0; i0 < len; i0 += D) {
+    double cur[D];
 #pragma unroll
-    for (int u = P; u >= 1; --u) v = fma(-__ldg(Li + u), y[u - 1], v);
-    v *= __ldg(Li);
+    for (int d = 0; d < D; ++d) cur[d] = nxt[d];
 #pragma unroll
-    for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
-    y[0] = v;
-    base[(long long)i * es] = v;
+    for (int d = 0; d < D; ++d) nxt[d] = (i0 + D + d < len) ? base[(long long)(i0 + D + d) * es] : 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int i = i0 + d;
+      if (i < len) {
+        double v = cur[d];
+        const double* Li = L + (long long)i * (P + 1);
+#pragma unroll
+        for (int u = P; u >= 1; --u) v = fma(-__ldg(Li + u), y[u - 1], v);
+        v *= __ldg(Li);
+#pragma unroll
+        for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+        y[0] = v;
+        base[(long long)i * es] = v;
+      }
+    }
   }
   // backward: z_i = (y_i - sum_{u=1..P} L_{i+u,i} z_{i+u}) / L_ii   (L padded with P zero rows)
 #pragma unroll
   for (int u = 0; u < P; ++u) y[u] = 0.0;
-  for (int i = len - 1; i >= 0; --i) {
-    double v = base[(long long)i * es];
 #pragma unroll
-    for (int u = P; u >= 1; --u) v = fma(-__ldg(L + (long long)(i + u) * (P + 1) + u), y[u - 1], v);
-    v *= __ldg(L + (long long)i * (P + 1));
+  for (int d = 0; d < D; ++d) nxt[d] = (len - 1 - d >= 0) ? base[(long long)(len - 1 - d) * es] : 0.0;
+  for (int i0 = len - 1; i0 >= 0; i0 -= D) {
+    double cur[D];
 #pragma unroll
-    for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
-    y[0] = v;
-    base[(long long)i * es] = v;
+    for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+#pragma unroll
+    for (int d = 0; d < D; ++d) nxt[d] = (i0 - D - d >= 0) ? base[(long long)(i0 - D - d) * es] : 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int i = i0 - d;
+      if (i >= 0) {
+        double v = cur[d];
+#pragma unroll
+        for (int u = P; u >= 1; --u) v = fma(-__ldg(L + (long long)(i + u) * (P + 1) + u), y[u - 1], v);
+        v *= __ldg(L + (long long)i * (P + 1));
+#pragma unroll
+        for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+        y[0] = v;
+        base[(long long)i * es] = v;
+      }
+    }
   }
 }
 
@@ -155,6 +188,176 @@ static void line_dispatch(int p, double* t, const double* L, int len, long long 
 #include "tile_core.cuh"
 
 namespace ga {
+
+// ---------------------------------------------------------------------------
+// Streaming line solver with fused PCG prologue/epilogue (single patch, many
+// lines: 3D).  One thread per (comp, line, rhs); consecutive threads are
+// consecutive (x, rhs) slots so y/z lines are coalesced.  The loads of the
+// next D elements are issued before the D recurrence steps of the current
+// block (software pipelining).  PRO: input = s o (r - alpha q) with
+// x += alpha p, r updated in place.  EPI: output z = s o (L^T)^{-1} y, with
+// the r.z / r.r partial sums and the PCG scalar step F1 in the last block.
+// ---------------------------------------------------------------------------
+struct LineArgs {
+  double* t;
+  const double* L;
+  int len;
+  long long es;
+  int na, nb, kk, nvec;
+  long long sa, sb, sc;
+  const double* s;
+  double *x, *r;
+  const double *p, *q;
+  PcgState* pcg;
+  DevStatus* st;
+  double* partial;
+  unsigned int* counter;
+  int maxit, update;
+  unsigned long long cond;
+};
+
+template <int P, bool PRO, bool EPI>
+__global__ void __launch_bounds__(NTHREADS) k_line_sf(LineArgs a) {
+  constexpr int D = (PRO || EPI) ? 8 : 16;
+  if (a.st->status != 0) return;  // uniform
+  count_launch(a.st);
+  const long long nl = (long long)a.nvec * a.nb * a.na * a.kk;
+  const long long l = (long long)gtid();
+  double acc[2 * KMAX];
+#pragma unroll
+  for (int q = 0; q < 2 * KMAX; ++q) acc[q] = 0.0;
+  if (l < nl) {
+    const int j = (int)(l % a.kk);
+    long long rem = l / a.kk;
+    const int ia = (int)(rem % a.na);
+    rem /= a.na;
+    const int ib = (int)(rem % a.nb);
+    const int c = (int)(rem / a.nb);
+    const long long pos = ib * a.sb + ia * a.sa;   // component-free offset of element 0
+    const long long o0 = c * a.sc + pos + j;         // offset of element 0 (relative to t, x, r, p, q)
+    const long long gp0 = pos / a.kk, ges = a.es / a.kk;
+    const int len = a.len;
+    const double* L = a.L;
+    double* t = a.t;
+    double al = 0.0;
+    bool upd = false;
+    if (PRO && a.update && !a.pcg->first) {
+      al = a.pcg->alpha[j];
+      upd = al != 0.0;
+    }
+    auto fetch_in = [&](int i) -> double {
+      const long long o = o0 + (long long)i * a.es;
+      if (PRO) {
+        double rv = a.r[o];
+        if (upd) {
+          const double xv = a.x[o], pv = a.p[o], qv = a.q[o];
+          a.x[o] = fma(al, pv, xv);
+          rv = fma(-al, qv, rv);
+          a.r[o] = rv;
+        }
+        return rv * a.s[gp0 + (long long)i * ges];
+      }
+      return t[o];
+    };
+    double y[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) y[u] = 0.0;
+    double nxt[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) nxt[d] = d < len ? fetch_in(d) : 0.0;
+    // forward: y_i = (t_i - sum_u L_{i,i-u} y_{i-u}) / L_ii
+    for (int i0 = 0; i0 < len; i0 += D) {
+      double cur[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+#pragma unroll
+      for (int d = 0; d < D; ++d) nxt[d] = (i0 + D + d < len) ? fetch_in(i0 + D + d) : 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int i = i0 + d;
+        if (i < len) {
+          double v = cur[d];
+          const double* Li = L + (long long)i * (P + 1);
+#pragma unroll
+          for (int u = P; u >= 1; --u) v = fma(-__ldg(Li + u), y[u - 1], v);
+          v *= __ldg(Li);
+#pragma unroll
+          for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+          y[0] = v;
+          t[o0 + (long long)i * a.es] = v;
+        }
+      }
+    }
+    // backward: z_i = (y_i - sum_u L_{i+u,i} z_{i+u}) / L_ii   (L padded with P zero rows)
+#pragma unroll
+    for (int u = 0; u < P; ++u) y[u] = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) nxt[d] = (len - 1 - d >= 0) ? t[o0 + (long long)(len - 1 - d) * a.es] : 0.0;
+    for (int i0 = len - 1; i0 >= 0; i0 -= D) {
+      double cur[D], sv[D], rv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+      if (EPI) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int i = i0 - d;
+          const long long ii = i >= 0 ? i : 0;
+          sv[d] = a.s[gp0 + ii * ges];
+          rv[d] = a.r[o0 + ii * a.es];
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) nxt[d] = (i0 - D - d >= 0) ? t[o0 + (long long)(i0 - D - d) * a.es] : 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int i = i0 - d;
+        if (i >= 0) {
+          double v = cur[d];
+#pragma unroll
+          for (int u = P; u >= 1; --u) v = fma(-__ldg(L + (long long)(i + u) * (P + 1) + u), y[u - 1], v);
+          v *= __ldg(L + (long long)i * (P + 1));
+#pragma unroll
+          for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+          y[0] = v;
+          if (EPI) {
+            const double z = v * sv[d];
+#pragma unroll
+            for (int q = 0; q < KMAX; ++q)
+              if (q == j) { acc[q] = fma(rv[d], z, acc[q]); acc[KMAX + q] = fma(rv[d], rv[d], acc[KMAX + q]); }
+            t[o0 + (long long)i * a.es] = z;
+          } else {
+            t[o0 + (long long)i * a.es] = v;
+          }
+        }
+      }
+    }
+  }
+  if (EPI) {
+    double out[2 * KMAX];
+    if (reduce_last_block<2 * KMAX>(acc, a.partial, a.counter, out))
+      pcg_finalize(a.pcg, a.st, a.kk, a.maxit, a.cond, out, out + KMAX);
+  }
+}
+
+template <int P>
+static void line_sf_launch(const LineArgs& a, bool pro, bool epi, cudaStream_t s) {
+  const long long nl = (long long)a.nvec * a.nb * a.na * a.kk;
+  const unsigned int blocks = (unsigned int)((nl + NTHREADS - 1) / NTHREADS);
+  if (pro) k_line_sf<P, true, false><<<blocks, NTHREADS, 0, s>>>(a);
+  else if (epi) k_line_sf<P, false, true><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_line_sf<P, false, false><<<blocks, NTHREADS, 0, s>>>(a);
+}
+static void line_sf_dispatch(int p, const LineArgs& a, bool pro, bool epi, cudaStream_t s) {
+  switch (p) {
+    case 1: line_sf_launch<1>(a, pro, epi, s); break;
+    case 2: line_sf_launch<2>(a, pro, epi, s); break;
+    case 3: line_sf_launch<3>(a, pro, epi, s); break;
+    case 4: line_sf_launch<4>(a, pro, epi, s); break;
+    case 5: line_sf_launch<5>(a, pro, epi, s); break;
+    case 6: line_sf_launch<6>(a, pro, epi, s); break;
+    default: line_sf_launch<7>(a, pro, epi, s); break;
+  }
+}
 
 template <int P>
 __global__ void __launch_bounds__(512) k_line_tile(TileLine a) {
@@ -292,8 +495,48 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
 void launch_precond(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
   const bool single = (a.npatch == 1 && a.t[0] == nullptr);
+  // line mode: tiles (chunked, shared memory; needed when lines are few, 2D)
+  // or streaming thread-per-line sweeps (many lines, 3D).  GA_LINE_MODE overrides.
+  static int line_mode = -1;  // 0 auto, 1 tile, 2 stream
+  if (line_mode < 0) {
+    const char* e = getenv("GA_LINE_MODE");
+    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : 0);
+  }
+  long long minslots = 1LL << 62;
+  for (int pr = 0; pr < a.npatch; ++pr)
+    for (int d = 0; d < g.dim; ++d) {
+      long long sl = (long long)a.nvec * a.kk;
+      for (int e2 = 0; e2 < g.dim; ++e2)
+        if (e2 != d) sl *= a.bd[pr][e2];
+      minslots = std::min(minslots, sl);
+    }
+  const bool stream = line_mode == 2 || (line_mode == 0 && minslots >= 148LL * 128);
+  if (single && stream) {
+    // streaming fused path (3D): first direction y (PRO, coalesced), then x, then z (EPI)
+    const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
+    const long long str[3] = {a.kk, (long long)g.nx * a.kk, (long long)g.nx * g.ny * a.kk};
+    const long long off = g.guard * a.kk;
+    int order[3] = {1, 0, 2};
+    if (g.dim == 2) { order[0] = 1; order[1] = 0; }
+    for (int k = 0; k < g.dim; ++k) {
+      const int d = order[k];
+      LineArgs la;
+      memset(&la, 0, sizeof(la));
+      la.t = a.z + off; la.L = a.L[0][d]; la.len = bd[d]; la.es = str[d]; la.kk = a.kk; la.nvec = a.nvec;
+      la.sc = g.padded * a.kk;
+      const int o1 = (d == 0) ? 1 : 0, o2 = (d == 2) ? 1 : 2;
+      la.na = bd[o1]; la.sa = str[o1];
+      la.nb = (g.dim == 3) ? bd[o2] : 1; la.sb = (g.dim == 3) ? str[o2] : 0;
+      la.s = a.s[0];
+      la.x = a.x + off; la.r = a.r + off; la.p = a.p0 + off; la.q = a.q + off;
+      la.pcg = a.pcg; la.st = a.st; la.partial = a.partial; la.counter = a.counter;
+      la.maxit = a.maxit; la.update = a.update; la.cond = a.cond;
+      line_sf_dispatch(a.p, la, k == 0, k == g.dim - 1, s);
+    }
+    return;
+  }
   // fused path: single patch, tile solver available for every direction
-  bool fused = single;
+  bool fused = single && !stream;
   for (int d = 0; d < g.dim && fused; ++d) fused = a.Ff[0][d] != nullptr && a.nchunk[0][d] <= 32;
   if (fused) {
     const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
@@ -350,7 +593,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     }
     for (int d = 0; d < g.dim; ++d) {
       bool done = false;
-      if (a.Ff[pr][d]) {
+      if (a.Ff[pr][d] && !stream) {
         TileLine tl;
         memset(&tl, 0, sizeof(tl));
         tl.t = t; tl.n = bd[d]; tl.kk = a.kk; tl.st = a.st;
