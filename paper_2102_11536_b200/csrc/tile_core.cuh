@@ -184,7 +184,7 @@ __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* t
                                         const double* pp, double* acc) {
   constexpr int TB = 4;
   const int n = a.n, ST = a.ST, nthr = blockDim.x, tid = threadIdx.x;
-  const int lgST = ST == 32 ? 5 : (ST == 16 ? 4 : 3);
+  const int lgST = 31 - __clz(ST);  // ST is a power of two (1..32)
   // tile geometry
   long long base = 0, gp0 = 0, ges = 0;
   int f0 = 0, nsl, sig0 = 0, l0 = 0, per = 1, tot;
