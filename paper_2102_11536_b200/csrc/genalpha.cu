@@ -432,6 +432,7 @@ PersistArgs persist_args(ga_ctx* ctx) {
   A.refine = ctx->d.pcg_refine;
   A.refine_rtol2 = ctx->d.pcg_refine_rtol > 0 ? ctx->d.pcg_refine_rtol * ctx->d.pcg_refine_rtol : 0.0;
   A.trace = ctx->trace;
+  A.p1 = ctx->pv1;
   return A;
 }
 

@@ -22,7 +22,9 @@ struct SpmvArgs {
   int mode;
   int fuse_p;          // SPMV_PQ: form p = z + beta p_old on the fly (x is ignored)
   const double* z;
-  double *p0, *p1;     // the two PCG direction buffers (parity of pcg->iter)
+  double *p0, *p1;     // fuse_p: p_old (read) and p_new (written) direction buffers
+  double fbeta[KMAX];  // fuse_p: beta of this iteration
+  int fpfirst;         // fuse_p: first iteration of the phase (p = z)
   double tol2, refine_rtol2;  // SPMV_TRUERES: thresholds of the refinement phase
   PcgState* pcg;
   DevStatus* st;
@@ -128,6 +130,7 @@ struct PersistArgs {
   int refine;
   double refine_rtol2;
   long long* trace;
+  double* p1;         // second direction buffer (fused direction update)
 };
 bool persist_supported(const PersistArgs& A);
 bool launch_pcg_persist(const PersistArgs& A, cudaStream_t s);

@@ -30,7 +30,7 @@ struct PersistDev {
   int fofs[3];          // offsets of the direction factors in shared memory
   int scratch_ofs;
   double* gpart;        // [2][gridDim][2*KMAX]
-  double *b, *x, *r, *z, *p;
+  double *b, *x, *r, *z, *p, *p1;   // p, p1: the two direction buffers (fused update)
   PcgState* pcg;
   DevStatus* st;
   long long* trace;     // optional phase timestamps (GA_TRACE): [iter][5] globaltimer ns
@@ -76,15 +76,15 @@ __device__ __forceinline__ void gsum(double (&v)[NV], double* gpart, int& buf, c
 
 template <int P, int KK>
 __device__ __forceinline__ void persist_precond(const PersistDev& A, double* smem, bool upd, const double* al,
-                                                double (&rz)[KK], double (&rr)[KK], int& gbuf, cg::grid_group& grid,
-                                                long long tslot = -1) {
+                                                const double* pnew_off, double (&rz)[KK], double (&rr)[KK], int& gbuf,
+                                                cg::grid_group& grid, long long tslot = -1) {
   double acc[2 * KMAX];
 #pragma unroll
   for (int j = 0; j < 2 * KMAX; ++j) acc[j] = 0.0;
   for (int d = 0; d < A.dim; ++d) {
     const TileLine& tl = A.tl[d];
     for (int t = blockIdx.x; t < A.ntiles[d]; t += gridDim.x)
-      tile_solve<P>(tl, t, smem + A.scratch_ofs, smem + A.fofs[d], upd && d == 0, al, tl.p0, acc);
+      tile_solve<P>(tl, t, smem + A.scratch_ofs, smem + A.fofs[d], upd && d == 0, al, pnew_off, acc);
     if (d < A.dim - 1) grid.sync();
     if (d == 0 && tslot >= 0) ptrace(A, tslot);
   }
@@ -143,6 +143,8 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
   for (int j = KK; j < KMAX; ++j) alpha[j] = 0.0;
   long long loops = 0;
   int status = 0, fail_block = -1;
+  double* pbuf[2] = {A.p, A.p1};
+  int par = 0;
   for (int phase = 0; phase < (A.refine ? 2 : 1); ++phase) {
     if (phase == 0) {
 #pragma unroll
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
     }
     bool first = true, pfirst = true;
     int iter = 0;
-    persist_precond<P, KK>(A, smem, false, alpha, rz, rr, gbuf, grid);
+    persist_precond<P, KK>(A, smem, false, alpha, pbuf[par] + g.guard * KK, rz, rr, gbuf, grid);
     for (;;) {
       // F1: convergence, beta
       int any = 0;
@@ -189,25 +191,23 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
         break;
       }
       ptrace(A, loops * 5 + 0);
-      // p = z (first) or z + beta p, active blocks
-      for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nel * KK; e += gstride) {
-        const int j = (int)(e % KK);
-        if (!active[j]) continue;
-        const long long ci = e / KK;
-        const long long i = ci % g.npts;
-        const int c = (int)(ci / g.npts);
-        const long long idx = ((long long)c * g.padded + g.guard + i) * KK + j;
-        const double zv = A.z[idx];
-        A.p[idx] = pfirst ? zv : fma(beta[j], A.p[idx], zv);
-      }
-      grid.sync();
       ptrace(A, loops * 5 + 1);
-      // q = M p, p.q
+      // q = M p with p = z + beta p_old formed on the SpMV input window (fused
+      // direction update, double-buffered p), p.q
+      SpmvArgs sq = A.spq;
+      sq.fuse_p = 1;
+      sq.z = A.z;
+      sq.p0 = pbuf[par];
+      sq.p1 = pbuf[par ^ 1];
+      sq.fpfirst = pfirst ? 1 : 0;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) sq.fbeta[j] = j < KK ? (active[j] ? beta[j] : 0.0) : 0.0;
       double pq[KK];
 #pragma unroll
       for (int j = 0; j < KK; ++j) pq[j] = 0.0;
       const long long nrg = ((g.npts + 31) / 32 + 7) / 8;
-      for (long long rb = blockIdx.x; rb < nrg; rb += gridDim.x) spmv_block<P, 1, KK, false, 8>(A.spq, rb, smem + A.scratch_ofs, pq);
+      for (long long rb = blockIdx.x; rb < nrg; rb += gridDim.x) spmv_block<P, 1, KK, false, 8>(sq, rb, smem + A.scratch_ofs, pq);
+      par ^= 1;
       gsum<KK>(pq, A.gpart, gbuf, grid);
       ptrace(A, loops * 5 + 2);
       ++iter;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
         if (active[j]) its[j] += 1;
       }
       // x += alpha p, r -= alpha q, z = calM^{-1} r, r.z, r.r
-      persist_precond<P, KK>(A, smem, true, alpha, rz, rr, gbuf, grid, (loops - 1) * 5 + 3);
+      persist_precond<P, KK>(A, smem, true, alpha, pbuf[par] + g.guard * KK, rz, rr, gbuf, grid, (loops - 1) * 5 + 3);
       ptrace(A, (loops - 1) * 5 + 4);
     }
     if (status != 0) break;
@@ -315,7 +315,7 @@ static bool persist_launch_t(const PersistArgs& A, cudaStream_t s) {
   D.tol2 = a.tol2; D.refine_rtol2 = A.refine_rtol2;
   D.spq = A.spq; D.str = A.str;
   D.gpart = a.partial;
-  D.b = A.va.b; D.x = a.x; D.r = a.r; D.z = a.z; D.p = const_cast<double*>(a.p0);
+  D.b = A.va.b; D.x = a.x; D.r = a.r; D.z = a.z; D.p = const_cast<double*>(a.p0); D.p1 = A.p1;
   D.pcg = a.pcg; D.st = a.st; D.trace = A.trace;
   for (int d = 0; d < 3; ++d) D.tl[d].trace = A.trace;
   static int max_blocks = -1;

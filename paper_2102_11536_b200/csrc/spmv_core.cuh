@@ -46,12 +46,23 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   const int P3 = (g.dim == 3) ? P : 0;
   const long long sy = g.nx, sz = (long long)g.nx * g.ny;
   const long long S = (long long)W * W * W3;
-  const double* __restrict__ xin = a.x;
+  const double* xin = a.x;
   const double* __restrict__ cslice = a.coef + (icl >> 5) * NCF * S * 32 + (icl & 31);
+  // fused PCG direction: the input window is p_new = z + beta p_old (z on the first iteration)
+  const bool fuse = a.mode == SPMV_PQ && a.fuse_p;
+  const bool mix = fuse && !a.fpfirst;
+  if (fuse) xin = a.z;
   auto fetch_win = [&](int line, int q, int c, double (&v)[KK]) {
     const int o3 = line / W - P3, o2 = line % W - P;
     const long long pos = g.guard + i0 - P + q + o3 * sz + o2 * sy;
-    load_row<KK>(xin + ((long long)c * g.padded + pos) * KK, v);
+    const long long e = ((long long)c * g.padded + pos) * KK;
+    load_row<KK>(xin + e, v);
+    if (mix) {
+      double po[KK];
+      load_row<KK>(a.p0 + e, po);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) v[j] = fma(a.fbeta[j], po[j], v[j]);
+    }
   };
   const int nlines = W3 * W;
   const bool two = r < 2 * P;
@@ -122,7 +133,21 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   for (int c = 0; c < NA; ++c) {
     const long long base = ((long long)c * g.padded + g.guard + i) * KK;
     double pv[KK];
-    if (a.mode == SPMV_PQ) load_row<KK>(a.x + base, pv);
+    if (a.mode == SPMV_PQ) {
+      if (fuse) {
+        load_row<KK>(a.z + base, pv);
+        if (mix) {
+          double po[KK];
+          load_row<KK>(a.p0 + base, po);
+#pragma unroll
+          for (int j = 0; j < KK; ++j) pv[j] = fma(a.fbeta[j], po[j], pv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < KK; ++j) a.p1[base + j] = pv[j];
+      } else {
+        load_row<KK>(a.x + base, pv);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
       double v = acc[c][j];

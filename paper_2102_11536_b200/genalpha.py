@@ -109,7 +109,7 @@ def ga_params(k, rho_b, rho_s=None, param_set=0):
 
 def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3, param_set=0,
               omega=1.0, lam=1.0, mu=1.0, density=1.0, pcg_rtol=1e-13, pcg_maxit=500,
-              pcg_refine=1, pcg_refine_rtol=None, unstable_factor=1e6):
+              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6):
     """ga_desc from [(cell, ctrl ndarray (m^dim, dim))].  Keeps the ctrl arrays
     alive on the returned object (`_keep`)."""
     arr = (ga_patch * len(patches))()
@@ -123,7 +123,9 @@ def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3,
     d = ga_desc(dim=dim, ncomp=ncomp, p=p, n=n, npatch=len(patches), patches=arr, omega=omega,
                 lame_lambda=lam, lame_mu=mu, density=density, k=k, rho_b=rho,
                 rho_s=rho if rho_s is None else rho_s, param_set=param_set, dt=dt,
-                pcg_rtol=pcg_rtol, pcg_maxit=pcg_maxit, pcg_refine=pcg_refine,
+                pcg_rtol=pcg_rtol, pcg_maxit=pcg_maxit,
+                # refinement restart (R8): needed where kappa(M) ~1e7-1e8 (3D p >= 5)
+                pcg_refine=(1 if p >= 5 else 0) if pcg_refine is None else pcg_refine,
                 pcg_refine_rtol=(1e-3 if p >= 5 else 0.0) if pcg_refine_rtol is None else pcg_refine_rtol,
                 unstable_factor=unstable_factor)
     d._keep = (arr, keep)
