@@ -168,6 +168,22 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- replicas
+def aggregate_replicas(local_ms, local_units, world, device=None):
+    """Multi-GPU = independent replicas: the job time is
+    the MAX of the ranks' device times, the work is the SUM of their units.
+    Returns (t_max_ms, total_units).  Only scalars cross ranks."""
+    if world <= 1:
+        return float(local_ms), float(local_units)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(local_ms)], dtype=torch.float64, device=device)
+    u = torch.tensor([float(local_units)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 # --------------------------------------------------------------------------- our arm
 def algorithmic_bytes(op, ctx_info):
     """Algorithmic (compulsory) bytes per launch, DESIGN.md "Roofline":
@@ -249,12 +265,8 @@ def run_ours(args, rank, world, local_rank):
     solves = st1.solves - st0.solves
     its = sum(st1.pcg_iters[j] - st0.pcg_iters[j] for j in range(4))
     n_free = ctx.n_free
-    t_max = ms
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(t.item())
-    value = world * n_free * args.steps / (t_max * 1e-3)
+    t_max, units = aggregate_replicas(ms, n_free * args.steps, world, dev)
+    value = units / (t_max * 1e-3)
 
     # ---- per-kernel timing (events on the launching stream, L2 flushed before each launch)
     info = dict(npts=n_free // nc if not cfg.get("lshape") else None, S=(2 * cfg["p"] + 1) ** cfg["dim"], nvec=nc,
@@ -336,12 +348,8 @@ def run_ours(args, rank, world, local_rank):
         u_host.copy_(u_dev, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e = {"value": world * n_free * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+    e2e_ms, e2e_units = aggregate_replicas(e0.elapsed_time(e1), n_free * args.steps, world, dev)
+    e2e = {"value": e2e_units / (e2e_ms * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": 8 * n_free / args.steps, "d2h_bytes_per_step": 8 * n_free,
            "note": "one job through the C ABI: pinned H2D of U0, ga_set_state (initial chain, "
                    f"{3 * cfg['k'] - 2} solves), then per step ga_advance(1) + D2H of U into pinned memory"}
