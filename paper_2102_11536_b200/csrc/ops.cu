@@ -63,6 +63,32 @@ __global__ void __launch_bounds__(NTHREADS) k_xr_prec_in(PrecArgs a) {
 }
 
 // multi-patch gather: t_r = s_r o R_r r on the box of patch r
+// all patches in one launch: element ranges of the patches are consecutive
+__global__ void __launch_bounds__(NTHREADS) k_prec_gather_all(PrecArgs a) {
+  if (a.st->status != 0) return;
+  count_launch(a.st);
+  const GridDesc g = a.g;
+  long long e = (long long)gtid();
+  int pr = 0;
+  for (; pr < a.npatch; ++pr) {
+    const long long n = (long long)a.nvec * a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2] * a.kk;
+    if (e < n) break;
+    e -= n;
+  }
+  if (pr >= a.npatch) return;
+  const int bx = a.bd[pr][0], by = a.bd[pr][1], bz = a.bd[pr][2];
+  const long long nbox = (long long)bx * by * bz;
+  const int j = (int)(e % a.kk);
+  const long long ci = e / a.kk;
+  const long long bi = ci % nbox;
+  const int c = (int)(ci / nbox);
+  const int ix = (int)(bi % bx), iy = (int)((bi / bx) % by), iz = (int)(bi / ((long long)bx * by));
+  const long long gi = (a.lo[pr][0] + ix) + (long long)g.nx * ((a.lo[pr][1] + iy) + (long long)g.ny * (a.lo[pr][2] + iz));
+  const double sv = a.s[pr][bi];
+  const double r = a.r[((long long)c * g.padded + g.guard + gi) * a.kk + j];
+  a.t[pr][((long long)c * nbox + bi) * a.kk + j] = sv * r;
+}
+
 __global__ void __launch_bounds__(NTHREADS) k_prec_gather(PrecArgs a, int pr) {
   if (a.st->status != 0) return;
   count_launch(a.st);
@@ -393,6 +419,36 @@ __global__ void __launch_bounds__(512) k_line_tile(TileLine a) {
   }
 }
 
+// Line tiles of several boxes (the patches of an additive Schwarz
+// preconditioner) in one launch: block b -> (patch, tile) by the prefix
+// table; every patch has its own factors and geometry, launch-wide ST.
+struct TileMulti {
+  TileLine tl[MAXPATCH];
+  int tstart[MAXPATCH + 1];
+  int np;
+};
+
+template <int P>
+__global__ void __launch_bounds__(512) k_line_tile_multi(TileMulti mt) {
+  int pr = 0;
+  while (pr + 1 < mt.np && (int)blockIdx.x >= mt.tstart[pr + 1]) ++pr;
+  const TileLine& a = mt.tl[pr];
+  if (a.st->status != 0) return;
+  if (blockIdx.x == 0) count_launch(a.st);
+  extern __shared__ double smem[];
+  const int n = a.n, ST = a.ST, LD = ST + 1;
+  double* Fs = smem + (size_t)n * LD + (size_t)a.C * P * ST;
+  for (int idx = threadIdx.x; idx < 2 * a.flen; idx += blockDim.x) Fs[idx] = idx < a.flen ? a.Ff[idx] : a.Fb[idx - a.flen];
+  double al[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) al[j] = 0.0;
+  double acc[2 * KMAX];
+#pragma unroll
+  for (int j = 0; j < 2 * KMAX; ++j) acc[j] = 0.0;
+  __syncthreads();
+  tile_solve<P>(a, (int)blockIdx.x - mt.tstart[pr], smem, Fs, false, al, a.p0, acc);
+}
+
 static size_t tile_smem(int n, int C, int p, int ST, int flen) {
   return sizeof(double) * ((size_t)n * (ST + 1) + (size_t)C * p * ST + 2 * (size_t)flen);
 }
@@ -435,6 +491,59 @@ static bool tile_dispatch(int p, const TileLine& a, cudaStream_t s) {
     case 5: return tile_launch<5>(a, s);
     case 6: return tile_launch<6>(a, s);
     default: return tile_launch<7>(a, s);
+  }
+}
+
+template <int P>
+static bool tile_multi_launch(TileMulti m, cudaStream_t s) {
+  // common slots per tile: the smallest any patch would use, <= 16 warps per block
+  int ST = 32, C = 1, nmax = 1, flen = 1;
+  long long tot32 = 0;
+  for (int r = 0; r < m.np; ++r) {
+    C = std::max(C, m.tl[r].C);
+    nmax = std::max(nmax, m.tl[r].n);
+    flen = std::max(flen, m.tl[r].flen);
+    if (m.tl[r].C > 32) return false;
+  }
+  auto ntiles_for = [&](const TileLine& t, int st) -> long long {
+    return t.mode == 0 ? (long long)t.nrows * ((t.rowlen + st - 1) / st) : ((long long)t.nlines * t.kk + st - 1) / st;
+  };
+  for (int r = 0; r < m.np; ++r) tot32 += ntiles_for(m.tl[r], 32);
+  if (tot32 < 296) {
+    long long tot16 = 0;
+    for (int r = 0; r < m.np; ++r) tot16 += ntiles_for(m.tl[r], 16);
+    ST = tot16 >= 148 ? 16 : 8;
+  }
+  while (ST > 8 && (C + 32 / ST - 1) / (32 / ST) > 16) ST >>= 1;
+  int t0 = 0;
+  for (int r = 0; r < m.np; ++r) {
+    m.tl[r].ST = ST;
+    m.tstart[r] = t0;
+    t0 += (int)ntiles_for(m.tl[r], ST);
+  }
+  m.tstart[m.np] = t0;
+  const size_t sm = tile_smem(nmax, C, P, ST, flen);
+  static size_t attr_max = 0;
+  if (sm + 4096 > 227 * 1024) return false;
+  if (sm > attr_max) {
+    if (cudaFuncSetAttribute(k_line_tile_multi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+      return false;
+    attr_max = sm;
+  }
+  const int cpw = 32 / ST;
+  const int nwarps = (C + cpw - 1) / cpw;
+  k_line_tile_multi<P><<<(unsigned int)t0, 32 * nwarps, sm, s>>>(m);
+  return true;
+}
+static bool tile_multi_dispatch(int p, const TileMulti& m, cudaStream_t s) {
+  switch (p) {
+    case 1: return tile_multi_launch<1>(m, s);
+    case 2: return tile_multi_launch<2>(m, s);
+    case 3: return tile_multi_launch<3>(m, s);
+    case 4: return tile_multi_launch<4>(m, s);
+    case 5: return tile_multi_launch<5>(m, s);
+    case 6: return tile_multi_launch<6>(m, s);
+    default: return tile_multi_launch<7>(m, s);
   }
 }
 
@@ -574,6 +683,50 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
   {
     const long long tot = (long long)a.nvec * g.npts * a.kk;
     k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+  }
+  if (!single && !stream) {
+    // batched Schwarz: one gather and one tile launch per direction for all patches
+    long long tot = 0;
+    for (int pr = 0; pr < a.npatch; ++pr) tot += (long long)a.nvec * a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2] * a.kk;
+    k_prec_gather_all<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+    bool ok = true;
+    for (int d = 0; d < g.dim && ok; ++d) {
+      TileMulti m;
+      memset(&m, 0, sizeof(m));
+      m.np = a.npatch;
+      for (int pr = 0; pr < a.npatch; ++pr) {
+        const int bd[3] = {a.bd[pr][0], a.bd[pr][1], a.bd[pr][2]};
+        const long long nbox = (long long)bd[0] * bd[1] * bd[2];
+        const long long str[3] = {a.kk, (long long)bd[0] * a.kk, (long long)bd[0] * bd[1] * a.kk};
+        const long long sc = nbox * a.kk;
+        TileLine& tl = m.tl[pr];
+        tl.t = a.t[pr]; tl.n = bd[d]; tl.kk = a.kk; tl.st = a.st;
+        tl.Ff = a.Ff[pr][d]; tl.Fb = a.Fb[pr][d]; tl.flen = a.flen[pr][d];
+        tl.clen = a.clen[pr][d]; tl.C = a.nchunk[pr][d]; tl.L = a.nlev[pr][d];
+        if (!tl.Ff) ok = false;
+        if (d == 0) {
+          tl.mode = 1; tl.nlines = a.nvec * bd[1] * bd[2]; tl.nl2 = bd[1] * bd[2]; tl.sA = sc; tl.sB = str[1];
+        } else {
+          tl.mode = 0; tl.es = str[d]; tl.rowlen = bd[0] * a.kk;
+          const int other = (d == 1) ? 2 : 1;
+          const int nother = (g.dim == 3) ? bd[other] : 1;
+          tl.nrows = a.nvec * nother; tl.nr2 = nother; tl.sA = sc; tl.sB = (g.dim == 3) ? str[other] : 0;
+        }
+      }
+      if (ok) ok = tile_multi_dispatch(a.p, m, s);
+    }
+    if (ok) {
+      const long long tot2 = (long long)a.nvec * g.npts;
+      const unsigned int nb = red_grid(tot2);
+      switch (a.kk) {
+        case 1: k_prec_out<1><<<nb, NTHREADS, 0, s>>>(a); break;
+        case 2: k_prec_out<2><<<nb, NTHREADS, 0, s>>>(a); break;
+        case 3: k_prec_out<3><<<nb, NTHREADS, 0, s>>>(a); break;
+        default: k_prec_out<4><<<nb, NTHREADS, 0, s>>>(a); break;
+      }
+      return;
+    }
+    // (fall through: per-patch path; the gather above is repeated harmlessly)
   }
   for (int pr = 0; pr < a.npatch; ++pr) {
     double* t;
