@@ -247,8 +247,18 @@ SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backwar
   F.clen = clen; F.C = C;
   // homogeneous responses H[i][u0-1] of chunk containing i to unit incoming state y_{a-u0}
   std::vector<double> H((size_t)n * p, 0.0);
+  // chunk w = [a, b): forward sweeps cut the line from index 0 (the short
+  // remainder chunk last); backward sweeps (reversed line) use the mirror
+  // image of that partition (short chunk first), so a thread that owns
+  // forward chunk w owns backward chunk C-1-w: the same elements.
+  const int rem = n - (C - 1) * clen;
+  auto bounds = [&](int w, int& a, int& b) {
+    if (!backward) { a = w * clen; b = std::min(n, a + clen); }
+    else { a = (w == 0) ? 0 : rem + (w - 1) * clen; b = (w == 0) ? rem : a + clen; }
+  };
   for (int w = 1; w < C; ++w) {
-    const int a = w * clen, b = std::min(n, a + clen);
+    int a, b;
+    bounds(w, a, b);
     for (int u0 = 1; u0 <= p; ++u0) {
       std::vector<double> h(b - a + p, 0.0);  // h[k] <-> index a - p + k
       h[p - u0] = 1.0;
@@ -269,7 +279,9 @@ SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backwar
   std::vector<double> A((size_t)std::max(L, 0) * C * p * p, 0.0);
   std::vector<double> cur((size_t)C * p * p, 0.0), nxt;
   for (int w = 0; w < E; ++w) {
-    const int a = w * clen, b = std::min(n, a + clen);
+    int a, b;
+    bounds(w, a, b);
+    (void)a;
     for (int u = 1; u <= p; ++u)
       for (int u0 = 1; u0 <= p; ++u0)
         cur[((size_t)w * p + (u - 1)) * p + (u0 - 1)] = (w == 0) ? 0.0 : H[(size_t)(b - u) * p + u0 - 1];

@@ -96,7 +96,11 @@ __device__ __forceinline__ void tile_sweep(double* __restrict__ tile, int LD, do
   const double* coef = F + n;
   const double* H = F + (size_t)n * (1 + P);
   const double* A = F + (size_t)n * (1 + 2 * P);
-  const int lo = ch * a.clen, hi = min(n, lo + a.clen);
+  // chunk bounds: forward from index 0 (short remainder last); backward = the
+  // mirror partition on the reversed line (short chunk first), host_math.cpp
+  const int rem = n - (a.C - 1) * a.clen;
+  const int lo = !rev ? ch * a.clen : (ch == 0 ? 0 : rem + (ch - 1) * a.clen);
+  const int hi = !rev ? min(n, lo + a.clen) : (ch == 0 ? rem : min(n, lo + a.clen));
   double y[P];
 #pragma unroll
   for (int u = 0; u < P; ++u) y[u] = 0.0;
