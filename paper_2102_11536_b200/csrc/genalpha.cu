@@ -902,8 +902,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     ctx->persist = want && persist_supported(persist_args(ctx));
     const char* te = getenv("GA_TRACE");
     if (te && *te && *te != '0') {
-      cudaMalloc(&ctx->trace, 4096 * sizeof(long long));  // debug only
-      cudaMemset(ctx->trace, 0, 4096 * sizeof(long long));
+      cudaMalloc(&ctx->trace, 8192 * sizeof(long long));  // debug only
+      cudaMemset(ctx->trace, 0, 8192 * sizeof(long long));
     }
   }
   if (!ctx->nograph) {
@@ -1165,7 +1165,7 @@ int ga_uses_persistent_solver(const ga_ctx* ctx) { return ctx && ctx->persist ? 
 // debug: copy the persistent-solver trace (GA_TRACE=1) to the host; returns slots copied
 int ga_debug_trace(ga_ctx* ctx, long long* host, int n) {
   if (!ctx || !ctx->trace || !host) return 0;
-  if (n > 4096) n = 4096;
+  if (n > 8192) n = 8192;
   if (cudaMemcpy(host, ctx->trace, sizeof(long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
 }

@@ -349,7 +349,11 @@ __global__ void __launch_bounds__(NTHREADS) k_line_sf(LineArgs a) {
             const double z = v * sv[d];
 #pragma unroll
             for (int q = 0; q < KMAX; ++q)
-              if (q == j) { acc[q] = fma(rv[d], z, acc[q]); acc[KMAX + q] = fma(rv[d], rv[d], acc[KMAX + q]); }
+              {  // branch-free (keeps acc in registers)
+                const double m = (q == j) ? rv[d] : 0.0;
+                acc[q] = fma(m, z, acc[q]);
+                acc[KMAX + q] = fma(m, rv[d], acc[KMAX + q]);
+              }
             t[o0 + (long long)i * a.es] = z;
           } else {
             t[o0 + (long long)i * a.es] = v;

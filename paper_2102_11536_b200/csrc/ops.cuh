@@ -25,6 +25,8 @@ struct SpmvArgs {
   double *p0, *p1;     // fuse_p: p_old (read) and p_new (written) direction buffers
   double fbeta[KMAX];  // fuse_p: beta of this iteration
   int fpfirst;         // fuse_p: first iteration of the phase (p = z)
+  double* fx;          // fuse_p and not first: also x += falpha p_old (the x update deferred from
+  double falpha[KMAX]; //   the previous iteration's preconditioner), null: off
   double tol2, refine_rtol2;  // SPMV_TRUERES: thresholds of the refinement phase
   PcgState* pcg;
   DevStatus* st;

@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
   for (int j = KK; j < KMAX; ++j) alpha[j] = 0.0;
   long long loops = 0;
   int status = 0, fail_block = -1;
-  double* pbuf[2] = {A.p, A.p1};
+  // the two direction buffers, selected without an indexed array (keeps them out of local memory)
+  auto pbuf = [&](int w) { return w ? A.p1 : A.p; };
   int par = 0;
   for (int phase = 0; phase < (A.refine ? 2 : 1); ++phase) {
     if (phase == 0) {
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
     }
     bool first = true, pfirst = true;
     int iter = 0;
-    persist_precond<P, KK>(A, smem, false, alpha, pbuf[par] + g.guard * KK, rz, rr, gbuf, grid);
+    persist_precond<P, KK>(A, smem, false, alpha, pbuf(par) + g.guard * KK, rz, rr, gbuf, grid);
     for (;;) {
       // F1: convergence, beta
       int any = 0;
@@ -197,11 +198,15 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
       SpmvArgs sq = A.spq;
       sq.fuse_p = 1;
       sq.z = A.z;
-      sq.p0 = pbuf[par];
-      sq.p1 = pbuf[par ^ 1];
+      sq.p0 = pbuf(par);
+      sq.p1 = pbuf(par ^ 1);
       sq.fpfirst = pfirst ? 1 : 0;
+      sq.fx = A.x;  // x += alpha_prev p_old on the own rows (deferred from the last preconditioner)
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) sq.fbeta[j] = j < KK ? (active[j] ? beta[j] : 0.0) : 0.0;
+      for (int j = 0; j < KMAX; ++j) {
+        sq.fbeta[j] = j < KK ? (active[j] ? beta[j] : 0.0) : 0.0;
+        sq.falpha[j] = j < KK ? alpha[j] : 0.0;
+      }
       double pq[KK];
 #pragma unroll
       for (int j = 0; j < KK; ++j) pq[j] = 0.0;
@@ -219,8 +224,21 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
         if (active[j]) its[j] += 1;
       }
       // x += alpha p, r -= alpha q, z = calM^{-1} r, r.z, r.r
-      persist_precond<P, KK>(A, smem, true, alpha, pbuf[par] + g.guard * KK, rz, rr, gbuf, grid, (loops - 1) * 5 + 3);
+      persist_precond<P, KK>(A, smem, true, alpha, pbuf(par) + g.guard * KK, rz, rr, gbuf, grid, (loops - 1) * 5 + 3);
       ptrace(A, (loops - 1) * 5 + 4);
+    }
+    if (iter > 0) {
+      // the last iteration's deferred x += alpha p (p = pbuf(par), the newest direction)
+      const double* pc = pbuf(par);
+      for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < g.npts * KK; e += gstride) {
+        const long long idx = g.guard * KK + e;
+        const int jj = (int)(e % KK);
+        double al = alpha[0];
+#pragma unroll
+        for (int q = 1; q < KK; ++q) al = (jj == q) ? alpha[q] : al;
+        if (al != 0.0) A.x[idx] = fma(al, pc[idx], A.x[idx]);
+      }
+      if (phase == 0 && A.refine && status == 0) grid.sync();  // the true residual reads x
     }
     if (status != 0) break;
   }
@@ -263,6 +281,7 @@ static inline TileLine fused_tile(const PrecArgs& a, int d, int ST) {
   tl.s = a.s[0];
   tl.x = a.x + off; tl.r = a.r + off; tl.p0 = a.p0 + off; tl.p1 = a.p0 + off; tl.q = a.q + off;
   tl.pcg = a.pcg; tl.maxit = a.maxit; tl.update = 1;
+  tl.xdefer = 1;  // x += alpha p rides on the next SpMV (and the exit pass)
   tl.pro = (d == 0);
   tl.epi = (d == g.dim - 1);
   return tl;

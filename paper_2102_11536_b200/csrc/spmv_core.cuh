@@ -139,6 +139,13 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
         if (mix) {
           double po[KK];
           load_row<KK>(a.p0 + base, po);
+          if (a.fx) {  // deferred x += alpha_prev p_old
+            double xv[KK];
+#pragma unroll
+            for (int j = 0; j < KK; ++j) xv[j] = a.fx[base + j];
+#pragma unroll
+            for (int j = 0; j < KK; ++j) a.fx[base + j] = fma(a.falpha[j], po[j], xv[j]);
+          }
 #pragma unroll
           for (int j = 0; j < KK; ++j) pv[j] = fma(a.fbeta[j], po[j], pv[j]);
         }

@@ -34,6 +34,7 @@ struct TileLine {
   int clen, C, L;
   // fusion (single patch; t is the z vector, offsets into x/r/p/q/s are the same)
   int pro, epi, update;
+  int xdefer;          // pro + update: skip x += alpha p (done by the next SpMV, persistent solver)
   const double* s;     // scaling per grid point
   long long padkk;     // padded * kk (component stride of an MV)
   double *x, *r;
@@ -85,6 +86,43 @@ static __device__ void pcg_finalize(PcgState* pc, DevStatus* st, int kk, int max
   if (condh) cudaGraphSetConditional((cudaGraphConditionalHandle)condh, cond ? 1u : 0u);
 }
 
+// Phase B of the chunked sweep: sigma_{w+1} = T_w sigma_w + tau_w over the
+// chunks w = 0..C-2 of every slot, Kogge-Stone in L levels through bsc
+// ([C][P][ST]); on return bsc[w] holds sigma_{w+1}.  ch is this thread's chunk
+// (>= C-1: no chunk state to contribute).  All threads of the block call it.
+template <int P>
+__device__ __forceinline__ void chunk_scan(double (&b)[P], double* __restrict__ bsc, const double* __restrict__ A,
+                                           int C, int L, int ST, int sl, int ch) {
+  const int E = C - 1;
+  for (int l = 0; l < L; ++l) {
+    const int d = 1 << l;
+    if (ch < E) {
+#pragma unroll
+      for (int u = 0; u < P; ++u) bsc[(ch * P + u) * ST + sl] = b[u];
+    }
+    __syncthreads();
+    if (ch < E && ch >= d) {
+      const double* Aw = A + ((size_t)l * C + ch) * P * P;
+      double bp[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) bp[u] = bsc[((ch - d) * P + u) * ST + sl];
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        double s2 = b[r];
+#pragma unroll
+        for (int c = 0; c < P; ++c) s2 = fma(Aw[r * P + c], bp[c], s2);
+        b[r] = s2;
+      }
+    }
+    __syncthreads();
+  }
+  if (ch < E) {
+#pragma unroll
+    for (int u = 0; u < P; ++u) bsc[(ch * P + u) * ST + sl] = b[u];
+  }
+  __syncthreads();
+}
+
 template <int P>
 __device__ __forceinline__ void tile_sweep(double* __restrict__ tile, int LD, double* __restrict__ bsc,
                                            const double* __restrict__ F, const TileLine& a, bool rev) {
@@ -117,37 +155,10 @@ __device__ __forceinline__ void tile_sweep(double* __restrict__ tile, int LD, do
     tile[pi * LD + sl] = v;
   }
   // phase B: sigma_{w+1} = T_w sigma_w + tau_w, w = 0..C-2, Kogge-Stone over chunks
-  const int E = a.C - 1;
   double b[P];
 #pragma unroll
   for (int u = 0; u < P; ++u) b[u] = y[u];  // tau_w[u] = y_{hi-1-u}
-  for (int l = 0; l < a.L; ++l) {
-    const int d = 1 << l;
-    if (ch < E) {
-#pragma unroll
-      for (int u = 0; u < P; ++u) bsc[(ch * P + u) * ST + sl] = b[u];
-    }
-    __syncthreads();
-    if (ch < E && ch >= d) {
-      const double* Aw = A + ((size_t)l * a.C + ch) * P * P;
-      double bp[P];
-#pragma unroll
-      for (int u = 0; u < P; ++u) bp[u] = bsc[((ch - d) * P + u) * ST + sl];
-#pragma unroll
-      for (int r = 0; r < P; ++r) {
-        double s2 = b[r];
-#pragma unroll
-        for (int c = 0; c < P; ++c) s2 = fma(Aw[r * P + c], bp[c], s2);
-        b[r] = s2;
-      }
-    }
-    __syncthreads();
-  }
-  if (ch < E) {
-#pragma unroll
-    for (int u = 0; u < P; ++u) bsc[(ch * P + u) * ST + sl] = b[u];
-  }
-  __syncthreads();
+  chunk_scan<P>(b, bsc, A, a.C, a.L, ST, sl, ch);
   // phase C: y_i += sum_u H_{i,u} sigma_ch[u]
   if (ch >= 1 && ch < a.C) {
     double sg[P];
@@ -253,7 +264,10 @@ __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* t
         if (a.pro) {
           v[u] = a.r[gg];
           sv[u] = a.s[gpp];
-          if (upd) { xv[u] = a.x[gg]; pv[u] = pp[gg]; qv[u] = a.q[gg]; }
+          if (upd) {
+            qv[u] = a.q[gg];
+            if (!a.xdefer) { xv[u] = a.x[gg]; pv[u] = pp[gg]; }
+          }
         } else {
           v[u] = a.t[gg];
         }
@@ -268,7 +282,7 @@ __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* t
 #pragma unroll
             for (int q = 1; q < KMAX; ++q) alj = (jj[u] == q) ? al[q] : alj;
             if (alj != 0.0) {
-              a.x[g[u]] = fma(alj, pv[u], xv[u]);
+              if (!a.xdefer) a.x[g[u]] = fma(alj, pv[u], xv[u]);
               w = fma(-alj, qv[u], w);
               a.r[g[u]] = w;
             }
@@ -295,12 +309,262 @@ __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* t
           w *= sv[u];
 #pragma unroll
           for (int q = 0; q < KMAX; ++q)
-            if (q == jj[u]) { acc[q] = fma(rv[u], w, acc[q]); acc[KMAX + q] = fma(rv[u], rv[u], acc[KMAX + q]); }
+            {  // branch-free (a data-dependent branch here turns acc into local memory)
+              const double m = (q == jj[u]) ? rv[u] : 0.0;
+              acc[q] = fma(m, w, acc[q]);
+              acc[KMAX + q] = fma(m, rv[u], acc[KMAX + q]);
+            }
         }
         a.t[g[u]] = w;
       }
     }
   }
+}
+
+// Register-resident variant of tile_solve (chunk length <= CL): each thread
+// loads the elements of its chunk straight from global memory into registers
+// (a thread that owns forward chunk w owns backward chunk C-1-w, the same
+// elements: mirror partition, host_math.cpp make_sweep), runs phases A and C
+// of both sweeps there and only exchanges the P-wide chunk states through
+// shared memory (chunk_scan).  Same arithmetic, in the same order, as the
+// shared-memory path.  Global accesses go in batches of 8 elements, all loads
+// of a batch before any store (the x/r/t pointers may alias as far as the
+// compiler knows).
+template <int P, int CL>
+__device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, double* smem, const double* Ff,
+                                               const double* Fb, bool upd, const double* al, const double* pp,
+                                               double* acc, unsigned long long* tprev) {
+  constexpr int BS = 4;
+  static_assert(CL % BS == 0, "CL must be a multiple of 4");
+  const int n = a.n, ST = a.ST, cpw = 32 / ST;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & (ST - 1);
+  const int ch = (threadIdx.x >> 5) * cpw + lane / ST;
+  double* bsc = smem;
+  // this thread's slot: element i at t[gb + i*gst], grid point gpb + i*gpst
+  long long gb, gpb, gst, gpst;
+  int j;
+  bool valid;
+  if (a.mode == 0) {
+    const int tpr = (a.rowlen + ST - 1) / ST;
+    const int r = tileid / tpr;
+    const int f = (tileid - r * tpr) * ST + sl;
+    valid = f < a.rowlen;
+    const long long roff = (long long)(r % a.nr2) * a.sB;
+    gb = (long long)(r / a.nr2) * a.sA + roff + f;
+    const int xo = div_kk(f, a.kk);
+    j = f - xo * a.kk;
+    gpb = roff / a.kk + xo;
+    gst = a.es;
+    gpst = a.es / a.kk;
+  } else {
+    const int sig = tileid * ST + sl;
+    valid = sig < a.nlines * a.kk;
+    const int ll = div_kk(sig, a.kk);
+    j = sig - ll * a.kk;
+    const int lq = ll / a.nl2;
+    const long long lr = (long long)(ll - lq * a.nl2) * a.sB;
+    gb = (long long)lq * a.sA + lr + j;
+    gpb = lr / a.kk;
+    gst = a.kk;
+    gpst = 1;
+  }
+  const int lo = ch * a.clen;
+  const int cnt = (valid && ch < a.C) ? min(n, lo + a.clen) - lo : 0;
+  gb += (long long)lo * gst;
+  gpb += (long long)lo * gpst;
+  double alj = 0.0;
+  if (upd) {
+    alj = al[0];
+#pragma unroll
+    for (int q = 1; q < KMAX; ++q) alj = (j == q) ? al[q] : alj;
+  }
+  auto tt = [&](int k) {
+    if (a.trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      long long* slot = a.trace + 4096 + blockIdx.x * 12 + (a.epi ? 6 : 0);
+      if (k > 0) slot[k - 1] += (long long)(t - *tprev);
+      else slot[5] += 1;
+      *tprev = t;
+    }
+  };
+  tt(0);
+  double v[CL];
+  // ---- load (+ fused PCG update x += alpha p, r -= alpha q, input scaling)
+  if (a.pro && upd && !a.xdefer) {
+#pragma unroll
+    for (int qb = 0; qb < CL; qb += BS) {
+      if (qb >= cnt) {
+#pragma unroll
+        for (int u = 0; u < BS; ++u) v[qb + u] = 0.0;
+        continue;
+      }
+      double rv[BS], sv[BS], xv[BS], pv[BS], qv[BS];
+#pragma unroll
+      for (int u = 0; u < BS; ++u) {
+        const bool ok = qb + u < cnt;
+        const long long g = ok ? gb + (long long)(qb + u) * gst : gb;
+        const long long gp = ok ? gpb + (long long)(qb + u) * gpst : gpb;
+        rv[u] = a.r[g];
+        sv[u] = a.s[gp];
+        xv[u] = a.x[g];
+        pv[u] = pp[g];
+        qv[u] = a.q[g];
+      }
+#pragma unroll
+      for (int u = 0; u < BS; ++u) {
+        double w = rv[u];
+        if (alj != 0.0 && qb + u < cnt) {
+          const long long g = gb + (long long)(qb + u) * gst;
+          a.x[g] = fma(alj, pv[u], xv[u]);
+          w = fma(-alj, qv[u], w);
+          a.r[g] = w;
+        }
+        v[qb + u] = w * sv[u];
+      }
+    }
+  } else if (a.pro) {
+    // every load of the chunk first (one memory round trip), then the r stores
+    double sv[CL], qv[CL];
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+      const bool ok = q < cnt;
+      v[q] = ok ? a.r[gb + (long long)q * gst] : 0.0;
+      sv[q] = ok ? a.s[gpb + (long long)q * gpst] : 0.0;
+      qv[q] = (ok && upd) ? a.q[gb + (long long)q * gst] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+      if (upd && alj != 0.0 && q < cnt) {
+        v[q] = fma(-alj, qv[q], v[q]);
+        a.r[gb + (long long)q * gst] = v[q];
+      }
+      v[q] *= sv[q];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < CL; ++q) v[q] = q < cnt ? a.t[gb + (long long)q * gst] : 0.0;
+  }
+  tt(1);
+  // ---- forward sweep L y = b
+  {
+    const double* dinv = Ff;
+    const double* coef = Ff + n;
+    const double* H = Ff + (size_t)n * (1 + P);
+    const double* A = Ff + (size_t)n * (1 + 2 * P);
+    double y[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) y[u] = 0.0;
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+      if (q < cnt) {
+        const int i = lo + q;
+        double w = v[q];
+#pragma unroll
+        for (int u = P; u >= 1; --u) w = fma(-coef[i * P + u - 1], y[u - 1], w);
+        w *= dinv[i];
+#pragma unroll
+        for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+        y[0] = w;
+        v[q] = w;
+      }
+    }
+    chunk_scan<P>(y, bsc, A, a.C, a.L, ST, sl, ch);
+    if (ch >= 1 && ch < a.C) {
+      double sg[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) sg[u] = bsc[((ch - 1) * P + u) * ST + sl];
+#pragma unroll
+      for (int q = 0; q < CL; ++q) {
+        if (q < cnt) {
+          const int i = lo + q;
+          double w = v[q];
+#pragma unroll
+          for (int u = 0; u < P; ++u) w = fma(H[i * P + u], sg[u], w);
+          v[q] = w;
+        }
+      }
+    }
+    __syncthreads();  // bsc is reused by the backward scan
+  }
+  tt(2);
+  // ---- backward sweep L^T z = y: forward sweep of the reversed line, chunk C-1-ch
+  {
+    const double* dinv = Fb;
+    const double* coef = Fb + n;
+    const double* H = Fb + (size_t)n * (1 + P);
+    const double* A = Fb + (size_t)n * (1 + 2 * P);
+    const int w = ch < a.C ? a.C - 1 - ch : a.C;
+    double y[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) y[u] = 0.0;
+#pragma unroll
+    for (int q = CL - 1; q >= 0; --q) {
+      if (q < cnt) {
+        const int i = n - 1 - (lo + q);
+        double x = v[q];
+#pragma unroll
+        for (int u = P; u >= 1; --u) x = fma(-coef[i * P + u - 1], y[u - 1], x);
+        x *= dinv[i];
+#pragma unroll
+        for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
+        y[0] = x;
+        v[q] = x;
+      }
+    }
+    chunk_scan<P>(y, bsc, A, a.C, a.L, ST, sl, w);
+    if (w >= 1 && w < a.C) {
+      double sg[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) sg[u] = bsc[((w - 1) * P + u) * ST + sl];
+#pragma unroll
+      for (int q = 0; q < CL; ++q) {
+        if (q < cnt) {
+          const int i = n - 1 - (lo + q);
+          double x = v[q];
+#pragma unroll
+          for (int u = 0; u < P; ++u) x = fma(H[i * P + u], sg[u], x);
+          v[q] = x;
+        }
+      }
+    }
+    __syncthreads();  // bsc is free for the next tile
+  }
+  tt(3);
+  // ---- store (+ output scaling and the r.z / r.r partials); loads first
+  double rz = 0.0, rr = 0.0;
+  if (a.epi) {
+    double rv[CL], sv[CL];
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+      const bool ok = q < cnt;
+      rv[q] = ok ? a.r[gb + (long long)q * gst] : 0.0;
+      sv[q] = ok ? a.s[gpb + (long long)q * gpst] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+      if (q < cnt) {
+        const double z = v[q] * sv[q];
+        rz = fma(rv[q], z, rz);
+        rr = fma(rv[q], rv[q], rr);
+        a.t[gb + (long long)q * gst] = z;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < CL; ++q)
+      if (q < cnt) a.t[gb + (long long)q * gst] = v[q];
+  }
+  if (a.epi) {
+#pragma unroll
+    for (int q = 0; q < KMAX; ++q)
+    {  // branch-free select (keeps acc in registers)
+      acc[q] += (q == j) ? rz : 0.0;
+      acc[KMAX + q] += (q == j) ? rr : 0.0;
+    }
+  }
+  tt(4);
 }
 
 // One tile (ST slots x the whole line) through shared memory: load (with the
@@ -310,14 +574,21 @@ __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* t
 template <int P>
 __device__ __forceinline__ void tile_solve(const TileLine& a, int tileid, double* smem, const double* Fs, bool upd,
                                            const double* al, const double* pp, double* acc) {
+  // GA_TRACE: per-block accumulated phase durations (ns) at trace[4096 + block*12 + (epi ? 6 : 0) + k]
+  unsigned long long tprev = 0;
+  if (a.clen <= 8) { tile_solve_reg<P, 8>(a, tileid, smem, Fs, Fs + a.flen, upd, al, pp, acc, &tprev); return; }
+  if (a.clen <= 16) { tile_solve_reg<P, 16>(a, tileid, smem, Fs, Fs + a.flen, upd, al, pp, acc, &tprev); return; }
   const int LD = a.ST + 1;
   double* tile = smem;
   double* bsc = tile + (size_t)a.n * LD;
   auto tt = [&](int k) {
-    if (a.trace && tileid == 0 && threadIdx.x == 0) {
+    if (a.trace && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.trace[4000 + (a.epi ? 5 : 0) + k] = (long long)t;
+      long long* slot = a.trace + 4096 + blockIdx.x * 12 + (a.epi ? 6 : 0);
+      if (k > 0) slot[k - 1] += (long long)(t - tprev);
+      else slot[5] += 1;
+      tprev = t;
     }
   };
   tt(0);
