@@ -262,8 +262,8 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
 }
 
 size_t sweep_bytes(int n, int p) {
-  // dinv + coef + H + A (L <= 5 levels, C <= 32 chunks)
-  return align256(sizeof(double) * ((size_t)n * (1 + 2 * p) + (size_t)5 * 32 * p * p));
+  // dinv + coef + H + A (L <= 6 levels, C <= 64 chunks)
+  return align256(sizeof(double) * ((size_t)n * (1 + 2 * p) + (size_t)6 * 64 * p * p));
 }
 
 Layout make_layout(const Shape& sh) {
@@ -859,11 +859,11 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       Lf.resize((size_t)(pp.bd[d] + sh.p + 1) * (sh.p + 1), 0.0);  // P zero rows for the backward sweep
       pp.hL[d] = Lf;
       pp.hdiag[d] = diag;
-      // chunks per line: enough threads (slots x chunks) to fill the GPU, <= 32
+      // chunks per line: enough threads (slots x chunks) to fill the GPU, <= 64
       long long slots = (long long)sh.nvec * sh.k;
       for (int e = 0; e < sh.dim; ++e)
         if (e != d) slots *= pp.bd[e];
-      const int ctarget = (int)std::max(2LL, std::min(32LL, (150000 + slots - 1) / slots));
+      const int ctarget = (int)std::max(2LL, std::min(64LL, (150000 + slots - 1) / slots));
       pp.sf[d] = make_sweep(Lf, pp.bd[d], sh.p, false, ctarget);
       pp.sb[d] = make_sweep(Lf, pp.bd[d], sh.p, true, ctarget);
       pp.Ff[d] = (double*)(ws + L.off_F[d][r]);

@@ -239,7 +239,7 @@ SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backwar
     }
   }
   if (chunks_target < 1) chunks_target = 1;
-  if (chunks_target > 32) chunks_target = 32;
+  if (chunks_target > 64) chunks_target = 64;
   int clen = (n + chunks_target - 1) / chunks_target;
   if (clen < p) clen = p;
   if (clen > n) clen = n;

@@ -459,7 +459,7 @@ static size_t tile_smem(int n, int C, int p, int ST, int flen) {
 
 template <int P>
 static bool tile_launch(TileLine a, cudaStream_t s) {
-  if (a.C > 32) return false;
+  if (a.C > 64) return false;
   const int nsl_total = a.mode == 0 ? -1 : a.nlines * a.kk;
   auto ntiles_for = [&](int st) -> long long {
     return a.mode == 0 ? (long long)a.nrows * ((a.rowlen + st - 1) / st) : ((long long)nsl_total + st - 1) / st;
@@ -507,7 +507,7 @@ static bool tile_multi_launch(TileMulti m, cudaStream_t s) {
     C = std::max(C, m.tl[r].C);
     nmax = std::max(nmax, m.tl[r].n);
     flen = std::max(flen, m.tl[r].flen);
-    if (m.tl[r].C > 32) return false;
+    if (m.tl[r].C > 64) return false;
   }
   auto ntiles_for = [&](const TileLine& t, int st) -> long long {
     return t.mode == 0 ? (long long)t.nrows * ((t.rowlen + st - 1) / st) : ((long long)t.nlines * t.kk + st - 1) / st;
@@ -650,7 +650,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
   }
   // fused path: single patch, tile solver available for every direction
   bool fused = single && !stream;
-  for (int d = 0; d < g.dim && fused; ++d) fused = a.Ff[0][d] != nullptr && a.nchunk[0][d] <= 32;
+  for (int d = 0; d < g.dim && fused; ++d) fused = a.Ff[0][d] != nullptr && a.nchunk[0][d] <= 64;
   if (fused) {
     const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
     const long long str[3] = {a.kk, (long long)g.nx * a.kk, (long long)g.nx * g.ny * a.kk};

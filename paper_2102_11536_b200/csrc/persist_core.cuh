@@ -36,6 +36,16 @@ struct PersistDev {
   long long* trace;     // optional phase timestamps (GA_TRACE): [iter][5] globaltimer ns
 };
 
+// GA_TRACE: per-block accumulated durations (SM cycles) at trace[6000 + block*4 + k]
+__device__ __forceinline__ void btrace(const PersistDev& A, int k, unsigned long long& tprev) {
+  if (A.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    t = (unsigned long long)clock64();  // SM cycles
+    if (k >= 0) A.trace[6000 + blockIdx.x * 4 + k] += (long long)(t - tprev);
+    tprev = t;
+  }
+}
+
 __device__ __forceinline__ void ptrace(const PersistDev& A, long long slot) {
   if (A.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 4096) {
     unsigned long long t;
@@ -84,7 +94,7 @@ __device__ __forceinline__ void persist_precond(const PersistDev& A, double* sme
   for (int d = 0; d < A.dim; ++d) {
     const TileLine& tl = A.tl[d];
     for (int t = blockIdx.x; t < A.ntiles[d]; t += gridDim.x)
-      tile_solve<P>(tl, t, smem + A.scratch_ofs, smem + A.fofs[d], upd && d == 0, al, pnew_off, acc);
+      tile_solve<P, 8>(tl, t, smem + A.scratch_ofs, smem + A.fofs[d], upd && d == 0, al, pnew_off, acc);
     if (d < A.dim - 1) grid.sync();
     if (d == 0 && tslot >= 0) ptrace(A, tslot);
   }
@@ -211,9 +221,15 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
 #pragma unroll
       for (int j = 0; j < KK; ++j) pq[j] = 0.0;
       const long long nrg = ((g.npts + 31) / 32 + 7) / 8;
+      unsigned long long tb = 0;
+      btrace(A, -1, tb);
       for (long long rb = blockIdx.x; rb < nrg; rb += gridDim.x) spmv_block<P, 1, KK, false, 8>(sq, rb, smem + A.scratch_ofs, pq);
+      btrace(A, 0, tb);
+      __syncthreads();
+      btrace(A, 1, tb);
       par ^= 1;
       gsum<KK>(pq, A.gpart, gbuf, grid);
+      btrace(A, 2, tb);
       ptrace(A, loops * 5 + 2);
       ++iter;
       ++loops;
@@ -292,14 +308,15 @@ static inline void persist_layout(const PersistArgs& Aa, PersistDev& D, size_t& 
   size_t ofs = 0;
   size_t scratch = 0;
   for (int d = 0; d < a.g.dim; ++d) {
-    // slots per tile so that 8 warps cover the chunks: 8 * (32/ST) >= C
+    // slots per tile so that 8 warps cover the chunks: 8 * (32/ST) >= C (C <= 64)
     const int C = a.nchunk[0][d];
     int ST = 32;
-    while (ST > 8 && 8 * (32 / ST) < C) ST >>= 1;
+    while (ST > 4 && 8 * (32 / ST) < C) ST >>= 1;
     D.tl[d] = fused_tile(a, d, ST);
     D.fofs[d] = (int)ofs;
     ofs += 2 * (size_t)a.flen[0][d];
-    const size_t tsz = (size_t)D.tl[d].n * (ST + 1) + (size_t)C * a.p * ST;
+    // register-resident tiles (clen <= 8) need only the chunk-state scratch
+    const size_t tsz = (a.clen[0][d] <= 8 ? 0 : (size_t)D.tl[d].n * (ST + 1)) + (size_t)C * a.p * ST;
     scratch = std::max(scratch, tsz);
     D.ntiles[d] = D.tl[d].mode == 0 ? D.tl[d].nrows * ((D.tl[d].rowlen + ST - 1) / ST)
                                     : (D.tl[d].nlines * D.tl[d].kk + ST - 1) / ST;
@@ -316,7 +333,7 @@ inline bool persist_supported_impl(const PersistArgs& A) {
   const PrecArgs& a = A.pa;
   if (a.npatch != 1 || a.t[0] != nullptr || a.nvec != 1) return false;
   for (int d = 0; d < a.g.dim; ++d)
-    if (!a.Ff[0][d] || a.nchunk[0][d] > 32) return false;
+    if (!a.Ff[0][d] || a.nchunk[0][d] > 64) return false;
   PersistDev D;
   size_t bytes = 0;
   persist_layout(A, D, bytes);

@@ -166,4 +166,6 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   }
 }
 
+
+
 }  // namespace ga

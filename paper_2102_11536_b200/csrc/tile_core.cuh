@@ -322,28 +322,33 @@ __device__ __forceinline__ void tile_io(const TileLine& a, int tileid, double* t
 }
 
 // Register-resident variant of tile_solve (chunk length <= CL): each thread
-// loads the elements of its chunk straight from global memory into registers
-// (a thread that owns forward chunk w owns backward chunk C-1-w, the same
-// elements: mirror partition, host_math.cpp make_sweep), runs phases A and C
-// of both sweeps there and only exchanges the P-wide chunk states through
-// shared memory (chunk_scan).  Same arithmetic, in the same order, as the
-// shared-memory path.  Global accesses go in batches of 8 elements, all loads
-// of a batch before any store (the x/r/t pointers may alias as far as the
-// compiler knows).
+// loads the elements of its chunk straight from global memory into the CL
+// register slots v[0..CL) (element lo+q in slot q; slots q >= cnt are dead)
+// and runs phases A and C of both sweeps there; only the P-wide chunk states
+// go through shared memory (chunk_scan).  A thread that owns forward chunk w
+// owns backward chunk C-1-w, the same elements (mirror partition,
+// host_math.cpp make_sweep).  Every register index is a compile-time constant
+// (the recurrence reads v[q-u] / v[q+u] directly, no shifted state array), so
+// v stays in registers; the sweeps are branch-free and read the factors at
+// fixed offsets from per-thread base pointers.  Dead slots compute finite
+// garbage in the forward sweep (after the live ones), are zeroed before the
+// backward sweep (which meets them first) and are never stored.  Factor
+// reads of dead slots may run up to CL elements past either end of a factor
+// buffer: they stay inside the adjacent [Ff | Fb] pair (finite values), which
+// every caller lays out contiguously.  Same arithmetic, in the same order, as
+// tile_sweep (the skipped terms multiply the zero incoming state).
 template <int P, int CL>
 __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, double* smem, const double* Ff,
                                                const double* Fb, bool upd, const double* al, const double* pp,
                                                double* acc, unsigned long long* tprev) {
-  constexpr int BS = 4;
-  static_assert(CL % BS == 0, "CL must be a multiple of 4");
-  const int n = a.n, ST = a.ST, cpw = 32 / ST;
+  const int n = a.n, ST = a.ST, cpw = 32 / ST, C = a.C;
   const int lane = threadIdx.x & 31;
   const int sl = lane & (ST - 1);
   const int ch = (threadIdx.x >> 5) * cpw + lane / ST;
   double* bsc = smem;
   // this thread's slot: element i at t[gb + i*gst], grid point gpb + i*gpst
-  long long gb, gpb, gst, gpst;
-  int j;
+  long long gb, gpb;
+  int gst, gpst, j;
   bool valid;
   if (a.mode == 0) {
     const int tpr = (a.rowlen + ST - 1) / ST;
@@ -355,8 +360,8 @@ __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, do
     const int xo = div_kk(f, a.kk);
     j = f - xo * a.kk;
     gpb = roff / a.kk + xo;
-    gst = a.es;
-    gpst = a.es / a.kk;
+    gst = (int)a.es;
+    gpst = (int)(a.es / a.kk);
   } else {
     const int sig = tileid * ST + sl;
     valid = sig < a.nlines * a.kk;
@@ -369,10 +374,12 @@ __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, do
     gst = a.kk;
     gpst = 1;
   }
-  const int lo = ch * a.clen;
-  const int cnt = (valid && ch < a.C) ? min(n, lo + a.clen) - lo : 0;
-  gb += (long long)lo * gst;
-  gpb += (long long)lo * gpst;
+  const bool live = valid && ch < C;
+  const int lo = live ? ch * a.clen : 0;
+  const int cnt = live ? min(n, lo + a.clen) - lo : 0;
+  double* __restrict__ tp = a.t + gb + (long long)lo * gst;
+  double* __restrict__ rp = a.r + gb + (long long)lo * gst;
+  const double* __restrict__ sp = a.s + gpb + (long long)lo * gpst;
   double alj = 0.0;
   if (upd) {
     alj = al[0];
@@ -382,7 +389,7 @@ __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, do
   auto tt = [&](int k) {
     if (a.trace && threadIdx.x == 0) {
       unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      t = (unsigned long long)clock64();  // SM cycles
       long long* slot = a.trace + 4096 + blockIdx.x * 12 + (a.epi ? 6 : 0);
       if (k > 0) slot[k - 1] += (long long)(t - *tprev);
       else slot[5] += 1;
@@ -392,155 +399,134 @@ __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, do
   tt(0);
   double v[CL];
   // ---- load (+ fused PCG update x += alpha p, r -= alpha q, input scaling)
-  if (a.pro && upd && !a.xdefer) {
-#pragma unroll
-    for (int qb = 0; qb < CL; qb += BS) {
-      if (qb >= cnt) {
-#pragma unroll
-        for (int u = 0; u < BS; ++u) v[qb + u] = 0.0;
-        continue;
-      }
-      double rv[BS], sv[BS], xv[BS], pv[BS], qv[BS];
-#pragma unroll
-      for (int u = 0; u < BS; ++u) {
-        const bool ok = qb + u < cnt;
-        const long long g = ok ? gb + (long long)(qb + u) * gst : gb;
-        const long long gp = ok ? gpb + (long long)(qb + u) * gpst : gpb;
-        rv[u] = a.r[g];
-        sv[u] = a.s[gp];
-        xv[u] = a.x[g];
-        pv[u] = pp[g];
-        qv[u] = a.q[g];
-      }
-#pragma unroll
-      for (int u = 0; u < BS; ++u) {
-        double w = rv[u];
-        if (alj != 0.0 && qb + u < cnt) {
-          const long long g = gb + (long long)(qb + u) * gst;
-          a.x[g] = fma(alj, pv[u], xv[u]);
-          w = fma(-alj, qv[u], w);
-          a.r[g] = w;
-        }
-        v[qb + u] = w * sv[u];
-      }
-    }
-  } else if (a.pro) {
-    // every load of the chunk first (one memory round trip), then the r stores
+  if (a.pro) {
+    const bool ur = upd && alj != 0.0;
+    const bool ux = ur && !a.xdefer;
+    double* __restrict__ xp = a.x + gb + (long long)lo * gst;
+    const double* __restrict__ qp = a.q + gb + (long long)lo * gst;
+    const double* __restrict__ ppp = pp + gb + (long long)lo * gst;
+    // every load of the chunk first (one memory round trip), then the stores
     double sv[CL], qv[CL];
 #pragma unroll
     for (int q = 0; q < CL; ++q) {
       const bool ok = q < cnt;
-      v[q] = ok ? a.r[gb + (long long)q * gst] : 0.0;
-      sv[q] = ok ? a.s[gpb + (long long)q * gpst] : 0.0;
-      qv[q] = (ok && upd) ? a.q[gb + (long long)q * gst] : 0.0;
+      v[q] = ok ? rp[q * gst] : 0.0;
+      sv[q] = ok ? sp[q * gpst] : 0.0;
+      qv[q] = (ok && ur) ? qp[q * gst] : 0.0;
+    }
+    if (ux) {
+#pragma unroll
+      for (int q0 = 0; q0 < CL; q0 += 4) {
+        double xv[4], pv[4];
+#pragma unroll
+        for (int u = 0; u < 4 && q0 + u < CL; ++u) {
+          const bool ok = q0 + u < cnt;
+          xv[u] = ok ? xp[(q0 + u) * gst] : 0.0;
+          pv[u] = ok ? ppp[(q0 + u) * gst] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4 && q0 + u < CL; ++u)
+          if (q0 + u < cnt) xp[(q0 + u) * gst] = fma(alj, pv[u], xv[u]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < CL; ++q) {
-      if (upd && alj != 0.0 && q < cnt) {
+      if (ur) {
         v[q] = fma(-alj, qv[q], v[q]);
-        a.r[gb + (long long)q * gst] = v[q];
+        if (q < cnt) rp[q * gst] = v[q];
       }
       v[q] *= sv[q];
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < CL; ++q) v[q] = q < cnt ? a.t[gb + (long long)q * gst] : 0.0;
+    for (int q = 0; q < CL; ++q) v[q] = q < cnt ? tp[q * gst] : 0.0;
   }
   tt(1);
-  // ---- forward sweep L y = b
+  // ---- forward sweep L y = b: element lo+q in slot q
   {
-    const double* dinv = Ff;
-    const double* coef = Ff + n;
-    const double* H = Ff + (size_t)n * (1 + P);
+    const double* fd = Ff + lo;                                    // dinv[lo+q]      = fd[q]
+    const double* fc = Ff + n + (size_t)lo * P;                    // coef[lo+q][u-1] = fc[q*P+u-1]
+    const double* fh = Ff + (size_t)n * (1 + P) + (size_t)lo * P;  // H[lo+q][u]      = fh[q*P+u]
     const double* A = Ff + (size_t)n * (1 + 2 * P);
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+      double w = v[q];
+#pragma unroll
+      for (int u = P; u >= 1; --u)
+        if (q - u >= 0) w = fma(-fc[q * P + u - 1], v[q - u], w);
+      v[q] = w * fd[q];
+    }
+    // outgoing state tau[u] = y_{hi-1-u} (zero before the chunk start)
     double y[P];
 #pragma unroll
     for (int u = 0; u < P; ++u) y[u] = 0.0;
 #pragma unroll
-    for (int q = 0; q < CL; ++q) {
-      if (q < cnt) {
-        const int i = lo + q;
-        double w = v[q];
+    for (int q = 0; q < CL; ++q)
 #pragma unroll
-        for (int u = P; u >= 1; --u) w = fma(-coef[i * P + u - 1], y[u - 1], w);
-        w *= dinv[i];
-#pragma unroll
-        for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
-        y[0] = w;
-        v[q] = w;
-      }
-    }
-    chunk_scan<P>(y, bsc, A, a.C, a.L, ST, sl, ch);
-    if (ch >= 1 && ch < a.C) {
+      for (int u = 0; u < P; ++u) y[u] = (q == cnt - 1 - u) ? v[q] : y[u];
+    chunk_scan<P>(y, bsc, A, C, a.L, ST, sl, ch);
+    if (ch >= 1 && ch < C) {
       double sg[P];
 #pragma unroll
       for (int u = 0; u < P; ++u) sg[u] = bsc[((ch - 1) * P + u) * ST + sl];
 #pragma unroll
       for (int q = 0; q < CL; ++q) {
-        if (q < cnt) {
-          const int i = lo + q;
-          double w = v[q];
+        double w = v[q];
 #pragma unroll
-          for (int u = 0; u < P; ++u) w = fma(H[i * P + u], sg[u], w);
-          v[q] = w;
-        }
+        for (int u = 0; u < P; ++u) w = fma(fh[q * P + u], sg[u], w);
+        v[q] = w;
       }
     }
+#pragma unroll
+    for (int q = 0; q < CL; ++q) v[q] = q < cnt ? v[q] : 0.0;  // dead slots: zero for the backward sweep
     __syncthreads();  // bsc is reused by the backward scan
   }
   tt(2);
-  // ---- backward sweep L^T z = y: forward sweep of the reversed line, chunk C-1-ch
+  // ---- backward sweep L^T z = y: forward sweep of the reversed line, i' = n-1-(lo+q), chunk C-1-ch
   {
-    const double* dinv = Fb;
-    const double* coef = Fb + n;
-    const double* H = Fb + (size_t)n * (1 + P);
+    const int ib = n - 1 - lo;
+    const double* fd = Fb + ib;                                    // dinv'[i']      = fd[-q]
+    const double* fc = Fb + n + (ptrdiff_t)ib * P;                 // coef'[i'][u-1] = fc[-q*P+u-1]
+    const double* fh = Fb + (size_t)n * (1 + P) + (ptrdiff_t)ib * P;  // H'[i'][u]   = fh[-q*P+u]
     const double* A = Fb + (size_t)n * (1 + 2 * P);
-    const int w = ch < a.C ? a.C - 1 - ch : a.C;
-    double y[P];
-#pragma unroll
-    for (int u = 0; u < P; ++u) y[u] = 0.0;
+    const int w = ch < C ? C - 1 - ch : C;
 #pragma unroll
     for (int q = CL - 1; q >= 0; --q) {
-      if (q < cnt) {
-        const int i = n - 1 - (lo + q);
-        double x = v[q];
+      double x = v[q];
 #pragma unroll
-        for (int u = P; u >= 1; --u) x = fma(-coef[i * P + u - 1], y[u - 1], x);
-        x *= dinv[i];
-#pragma unroll
-        for (int u = P - 1; u >= 1; --u) y[u] = y[u - 1];
-        y[0] = x;
-        v[q] = x;
-      }
+      for (int u = P; u >= 1; --u)
+        if (q + u <= CL - 1) x = fma(-fc[-q * P + u - 1], v[q + u], x);
+      v[q] = x * fd[-q];
     }
-    chunk_scan<P>(y, bsc, A, a.C, a.L, ST, sl, w);
-    if (w >= 1 && w < a.C) {
+    // outgoing state: the last P live elements in reversed order are slots 0..P-1
+    double y[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) y[u] = (u < cnt) ? v[u] : 0.0;
+    chunk_scan<P>(y, bsc, A, C, a.L, ST, sl, w);
+    if (w >= 1 && w < C) {
       double sg[P];
 #pragma unroll
       for (int u = 0; u < P; ++u) sg[u] = bsc[((w - 1) * P + u) * ST + sl];
 #pragma unroll
       for (int q = 0; q < CL; ++q) {
-        if (q < cnt) {
-          const int i = n - 1 - (lo + q);
-          double x = v[q];
+        double x = v[q];
 #pragma unroll
-          for (int u = 0; u < P; ++u) x = fma(H[i * P + u], sg[u], x);
-          v[q] = x;
-        }
+        for (int u = 0; u < P; ++u) x = fma(fh[-q * P + u], sg[u], x);
+        v[q] = x;
       }
     }
     __syncthreads();  // bsc is free for the next tile
   }
   tt(3);
   // ---- store (+ output scaling and the r.z / r.r partials); loads first
-  double rz = 0.0, rr = 0.0;
   if (a.epi) {
+    double rz = 0.0, rr = 0.0;
     double rv[CL], sv[CL];
 #pragma unroll
     for (int q = 0; q < CL; ++q) {
       const bool ok = q < cnt;
-      rv[q] = ok ? a.r[gb + (long long)q * gst] : 0.0;
-      sv[q] = ok ? a.s[gpb + (long long)q * gpst] : 0.0;
+      rv[q] = ok ? rp[q * gst] : 0.0;
+      sv[q] = ok ? sp[q * gpst] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < CL; ++q) {
@@ -548,21 +534,18 @@ __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, do
         const double z = v[q] * sv[q];
         rz = fma(rv[q], z, rz);
         rr = fma(rv[q], rv[q], rr);
-        a.t[gb + (long long)q * gst] = z;
+        tp[q * gst] = z;
       }
+    }
+#pragma unroll
+    for (int q = 0; q < KMAX; ++q) {  // branch-free select (keeps acc in registers)
+      acc[q] += (q == j) ? rz : 0.0;
+      acc[KMAX + q] += (q == j) ? rr : 0.0;
     }
   } else {
 #pragma unroll
     for (int q = 0; q < CL; ++q)
-      if (q < cnt) a.t[gb + (long long)q * gst] = v[q];
-  }
-  if (a.epi) {
-#pragma unroll
-    for (int q = 0; q < KMAX; ++q)
-    {  // branch-free select (keeps acc in registers)
-      acc[q] += (q == j) ? rz : 0.0;
-      acc[KMAX + q] += (q == j) ? rr : 0.0;
-    }
+      if (q < cnt) tp[q * gst] = v[q];
   }
   tt(4);
 }
@@ -571,20 +554,23 @@ __device__ __forceinline__ void tile_solve_reg(const TileLine& a, int tileid, do
 // optional fused PCG update / input scaling), forward and backward chunked
 // sweeps, store (with the optional output scaling and r.z / r.r partials in
 // acc).  All threads of the block call it; factors already in Fs.
-template <int P>
+template <int P, int CLMAX = 12>
 __device__ __forceinline__ void tile_solve(const TileLine& a, int tileid, double* smem, const double* Fs, bool upd,
                                            const double* al, const double* pp, double* acc) {
-  // GA_TRACE: per-block accumulated phase durations (ns) at trace[4096 + block*12 + (epi ? 6 : 0) + k]
+  // GA_TRACE: per-block accumulated phase durations (SM cycles) at trace[4096 + block*12 + (epi ? 6 : 0) + k]
   unsigned long long tprev = 0;
+  if (a.clen <= 4) { tile_solve_reg<P, 4>(a, tileid, smem, Fs, Fs + a.flen, upd, al, pp, acc, &tprev); return; }
   if (a.clen <= 8) { tile_solve_reg<P, 8>(a, tileid, smem, Fs, Fs + a.flen, upd, al, pp, acc, &tprev); return; }
-  if (a.clen <= 16) { tile_solve_reg<P, 16>(a, tileid, smem, Fs, Fs + a.flen, upd, al, pp, acc, &tprev); return; }
+  if constexpr (CLMAX >= 12) {
+    if (a.clen <= 12) { tile_solve_reg<P, 12>(a, tileid, smem, Fs, Fs + a.flen, upd, al, pp, acc, &tprev); return; }
+  }
   const int LD = a.ST + 1;
   double* tile = smem;
   double* bsc = tile + (size_t)a.n * LD;
   auto tt = [&](int k) {
     if (a.trace && threadIdx.x == 0) {
       unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      t = (unsigned long long)clock64();  // SM cycles
       long long* slot = a.trace + 4096 + blockIdx.x * 12 + (a.epi ? 6 : 0);
       if (k > 0) slot[k - 1] += (long long)(t - tprev);
       else slot[5] += 1;

@@ -1,0 +1,109 @@
+// Microbenchmarks of the latencies the small-problem solver is built from
+// (dependent DFMA, LDS, __syncthreads at 256 threads, shuffle, L2 pointer chase,
+// grid-wide barrier).  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/ubench.cu -o /tmp/ubench
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <vector>
+namespace cg = cooperative_groups;
+
+__global__ void k_dfma(double* out, long long* cyc, int n) {
+  double a = threadIdx.x * 1e-3, b = 1.0000001, c = 1e-9;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) a = fma(a, b, c);
+  long long t1 = clock64();
+  out[threadIdx.x] = a;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void k_lds(double* out, long long* cyc, int n) {
+  __shared__ int nxt[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) nxt[i] = (i * 97 + 13) & 1023;
+  __syncthreads();
+  int p = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) p = nxt[p];
+  long long t1 = clock64();
+  out[threadIdx.x] = p;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void k_sync(double* out, long long* cyc, int n) {
+  __shared__ double s[1024];
+  double a = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    s[threadIdx.x] = a + i;
+    __syncthreads();
+    a += s[(threadIdx.x + 1) & (blockDim.x - 1)];
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = a;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void k_shfl(double* out, long long* cyc, int n) {
+  double a = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) a = __shfl_up_sync(0xffffffffu, a, 1) + 1.0;
+  long long t1 = clock64();
+  out[threadIdx.x] = a;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void k_chase(const long long* nxt, double* out, long long* cyc, int n) {
+  long long p = threadIdx.x * 33;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) p = nxt[p];
+  long long t1 = clock64();
+  out[threadIdx.x] = (double)p;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void k_grid(double* out, long long* cyc, int n) {
+  cg::grid_group g = cg::this_grid();
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) g.sync();
+  long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+int main() {
+  double* out;
+  long long* cyc;
+  long long h;
+  cudaMalloc(&out, 1 << 20);
+  cudaMalloc(&cyc, 64);
+  const int n = 4096;
+  auto rep = [&](const char* name, int per) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-28s %8.1f cycles\n", name, (double)h / (n * per));
+  };
+  k_dfma<<<1, 32>>>(out, cyc, n);  k_dfma<<<1, 32>>>(out, cyc, n);  rep("dependent DFMA (1 warp)", 1);
+  k_dfma<<<1, 256>>>(out, cyc, n); rep("dependent DFMA (8 warps)", 1);
+  k_lds<<<1, 32>>>(out, cyc, n);   rep("dependent LDS.32 (1 warp)", 1);
+  k_sync<<<1, 256>>>(out, cyc, n); rep("st+sync+ld+sync (8 warps)", 1);
+  k_sync<<<1, 512>>>(out, cyc, n); rep("st+sync+ld+sync (16 warps)", 1);
+  k_shfl<<<1, 32>>>(out, cyc, n);  rep("dependent shfl+add", 1);
+  // L2 pointer chase over 32 MB (L2 resident after a warm pass)
+  const long long N = 4 << 20;
+  std::vector<long long> hn(N);
+  for (long long i = 0; i < N; ++i) hn[i] = (i * 1000003 + 7919) % N;
+  long long* dn;
+  cudaMalloc(&dn, N * 8);
+  cudaMemcpy(dn, hn.data(), N * 8, cudaMemcpyHostToDevice);
+  k_chase<<<1, 1>>>(dn, out, cyc, n);
+  k_chase<<<1, 1>>>(dn, out, cyc, n); rep("L2 pointer chase (32 MB)", 1);
+  int dev = 0, nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int nn = 256;
+  void* args[] = {&out, &cyc, &nn};
+  for (int b : {1, 2}) {
+    cudaLaunchCooperativeKernel((void*)k_grid, dim3(nsm * b), dim3(256), args, 0, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("grid.sync (%d blocks x 256)    %8.1f cycles\n", nsm * b, (double)h / nn);
+  }
+  return 0;
+}
