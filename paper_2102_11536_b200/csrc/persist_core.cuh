@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(PBLK) k_pcg_persist(PersistDev A) {
       par ^= 1;
       gsum<KK>(pq, A.gpart, gbuf, grid);
       btrace(A, 2, tb);
+      if (A.trace && threadIdx.x == 0) A.trace[6000 + blockIdx.x * 4 + 3] += 1950;  // count (x 1950: the script divides by cycles/us)
       ptrace(A, loops * 5 + 2);
       ++iter;
       ++loops;

@@ -52,17 +52,17 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   const bool fuse = a.mode == SPMV_PQ && a.fuse_p;
   const bool mix = fuse && !a.fpfirst;
   if (fuse) xin = a.z;
-  auto fetch_win = [&](int line, int q, int c, double (&v)[KK]) {
+  // raw window loads (the p_old part is combined when the window is staged,
+  // one line later, so the prefetch really overlaps the current line)
+  auto fetch_win = [&](int line, int q, int c, double (&v)[KK], double (&vo)[KK]) {
     const int o3 = line / W - P3, o2 = line % W - P;
     const long long pos = g.guard + i0 - P + q + o3 * sz + o2 * sy;
     const long long e = ((long long)c * g.padded + pos) * KK;
     load_row<KK>(xin + e, v);
-    if (mix) {
-      double po[KK];
-      load_row<KK>(a.p0 + e, po);
-#pragma unroll
-      for (int j = 0; j < KK; ++j) v[j] = fma(a.fbeta[j], po[j], v[j]);
-    }
+    if (mix) load_row<KK>(a.p0 + e, vo);
+  };
+  auto staged = [&](const double (&v)[KK], const double (&vo)[KK], int j) {
+    return mix ? fma(a.fbeta[j], vo[j], v[j]) : v[j];
   };
   const int nlines = W3 * W;
   const bool two = r < 2 * P;
@@ -71,12 +71,12 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   for (int c = 0; c < NA; ++c)
 #pragma unroll
     for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
-  double pw[2][NB][KK];
+  double pw[2][NB][KK], po[2][NB][KK];
   double cf[ELASTIC ? 1 : W];
 #pragma unroll
   for (int c = 0; c < NB; ++c) {
-    fetch_win(0, r, c, pw[0][c]);
-    if (two) fetch_win(0, BR + r, c, pw[1][c]);
+    fetch_win(0, r, c, pw[0][c], po[0][c]);
+    if (two) fetch_win(0, BR + r, c, pw[1][c], po[1][c]);
   }
   if constexpr (!ELASTIC) {
 #pragma unroll
@@ -88,8 +88,8 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
     for (int c = 0; c < NB; ++c)
 #pragma unroll
       for (int j = 0; j < KK; ++j) {
-        win[gq][buf][c][r][j] = pw[0][c][j];
-        if (two) win[gq][buf][c][BR + r][j] = pw[1][c][j];
+        win[gq][buf][c][r][j] = staged(pw[0][c], po[0][c], j);
+        if (two) win[gq][buf][c][BR + r][j] = staged(pw[1][c], po[1][c], j);
       }
     double ccur[ELASTIC ? 1 : W];
     if constexpr (!ELASTIC) {
@@ -100,8 +100,8 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
     if (line + 1 < nlines) {
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        fetch_win(line + 1, r, c, pw[0][c]);
-        if (two) fetch_win(line + 1, BR + r, c, pw[1][c]);
+        fetch_win(line + 1, r, c, pw[0][c], po[0][c]);
+        if (two) fetch_win(line + 1, BR + r, c, pw[1][c], po[1][c]);
       }
       if constexpr (!ELASTIC) {
 #pragma unroll

@@ -25,6 +25,7 @@ for nm, o in (("x", 0), ("y", 6)):
     print("tile %s (%d blocks, %.1f tiles each): load %.2f fwd %.2f bwd %.2f store %.2f  | max over blocks: %.2f %.2f %.2f %.2f" % (
         (nm, act.sum(), cnt[act].mean()) + tuple(per.mean(0)) + tuple(per.max(0))))
 
-sb = np.array(buf[6000:6000 + 148 * 4]).reshape(148, 4) / 1950.0 / max(1, 4 * len(t))  # 4 steps ran (kbench preamble 3 + 1)
-print("per block totals over the traced step / iterations: spmv-own(thread0) mean %.2f max %.2f | block barrier mean %.2f | gsum mean %.2f max %.2f" % (
+sb = np.array(buf[6000:6000 + 148 * 4]).reshape(148, 4) / 1950.0
+sb = sb[:, :3] / sb[:, 3:4]  # per SpMV call, us
+print("per SpMV call: own row-blocks mean %.2f max %.2f | block barrier %.2f | gsum mean %.2f max %.2f us" % (
     sb[:, 0].mean(), sb[:, 0].max(), sb[:, 1].mean(), sb[:, 2].mean(), sb[:, 2].max()))

@@ -68,6 +68,65 @@ __global__ void k_grid(double* out, long long* cyc, int n) {
   if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+
+// flat sense-reversal barrier: one counter, generation word
+__device__ __forceinline__ void flat_barrier(unsigned int* cnt, volatile unsigned int* gen, unsigned int nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g0 = *gen;
+    __threadfence();
+    if (atomicAdd(cnt, 1u) == nb - 1) {
+      *cnt = 0;
+      __threadfence();
+      atomicAdd((unsigned int*)gen, 1u);
+    } else {
+      unsigned int g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen));
+      } while (g == g0);
+    }
+  }
+  __syncthreads();
+}
+__global__ void k_flat(unsigned int* cnt, unsigned int* gen, long long* cyc, int n) {
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) flat_barrier(cnt, gen, gridDim.x);
+  long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+// two-level: groups of G blocks arrive on a group counter; the last of a group arrives on the top counter
+__device__ __forceinline__ void tree_barrier(unsigned int* cnt, volatile unsigned int* gen, unsigned int nb, int G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g0 = *gen;
+    __threadfence();
+    const unsigned int grp = blockIdx.x / G, ngrp = (nb + G - 1) / G;
+    const unsigned int gsz = min((unsigned)G, nb - grp * G);
+    bool last = false;
+    if (atomicAdd(cnt + 1 + grp * 32, 1u) == gsz - 1) {
+      cnt[1 + grp * 32] = 0;
+      if (atomicAdd(cnt, 1u) == ngrp - 1) last = true;
+    }
+    if (last) {
+      *cnt = 0;
+      __threadfence();
+      atomicAdd((unsigned int*)gen, 1u);
+    } else {
+      unsigned int g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen));
+      } while (g == g0);
+    }
+  }
+  __syncthreads();
+}
+__global__ void k_tree(unsigned int* cnt, unsigned int* gen, long long* cyc, int n, int G) {
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) tree_barrier(cnt, gen, gridDim.x, G);
+  long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
 int main() {
   double* out;
   long long* cyc;
@@ -104,6 +163,26 @@ int main() {
     cudaDeviceSynchronize();
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("grid.sync (%d blocks x 256)    %8.1f cycles\n", nsm * b, (double)h / nn);
+  }
+
+  unsigned int* cnt;
+  cudaMalloc(&cnt, 1 << 16);
+  cudaMemset(cnt, 0, 1 << 16);
+  unsigned int* gen = cnt + 8192;
+  {
+    void* a2[] = {&cnt, &gen, &cyc, &nn};
+    cudaLaunchCooperativeKernel((void*)k_flat, dim3(nsm), dim3(256), a2, 0, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("flat barrier (%d blocks)       %8.1f cycles  (%s)\n", nsm, (double)h / nn, cudaGetErrorString(cudaGetLastError()));
+    for (int G : {8, 12, 16}) {
+      cudaMemset(cnt, 0, 1 << 16);
+      void* a3[] = {&cnt, &gen, &cyc, &nn, &G};
+      cudaLaunchCooperativeKernel((void*)k_tree, dim3(nsm), dim3(256), a3, 0, 0);
+      cudaDeviceSynchronize();
+      cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+      printf("tree barrier G=%2d              %8.1f cycles  (%s)\n", G, (double)h / nn, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   return 0;
 }
