@@ -90,6 +90,11 @@ typedef struct {
                         /*    (x0 = main-phase result; reaching pcg_maxit here is not   */
                         /*    an error).  1e-3 recommended for p >= 5 (kappa(M) ~1e8)   */
   double unstable_factor; /* GA_ERR_UNSTABLE threshold on ||U||/||U_0||; 0 disables   */
+  int op_mode;          /* operator representation: */
+                        /* 1: assembled column-index-free stencils (2p+1)^dim per row;  */
+                        /* 2: matrix-free sum factorisation from the Gauss-point data   */
+                        /*    (single patch only; the elastic K stays a stencil);       */
+                        /* 0: auto = the measured-faster of the two      */
 } ga_desc;
 
 typedef struct {
@@ -185,6 +190,8 @@ ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
 /* Persistent-solver mode: 1 if ga_create chose the single-kernel cooperative PCG
  * solve (small single-patch scalar problems; env GA_PERSIST=0/1 overrides). */
 int ga_uses_persistent_solver(const ga_ctx* ctx);
+/* 1 if the context applies M (and the scalar K) matrix-free (op_mode 2, or op_mode 0's pick). */
+int ga_uses_matrix_free(const ga_ctx* ctx);
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream);
 
 void ga_destroy(ga_ctx* ctx);

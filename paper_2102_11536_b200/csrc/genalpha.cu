@@ -76,6 +76,9 @@ struct ga_ctx {
   std::string err;
   bool nograph = false;  // GA_NO_GRAPH=1: direct launches, host-driven PCG loop (profiling/debug)
   bool persist = false;  // small single-patch scalar problems: one cooperative kernel per solve
+  bool mf = false;       // matrix-free M (and scalar K): sum factorisation from Gauss-point data
+  double *mfWM = nullptr, *mfWK = nullptr, *mftv = nullptr, *mftd = nullptr, *diagM = nullptr;
+  long long mfws = 0;    // Gauss points (n(p+1))^dim
   long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
 };
 
@@ -99,7 +102,7 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t off_coefM, off_coefK, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
-      off_dscal;
+      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
 };
@@ -115,7 +118,10 @@ struct Shape {
   std::vector<long long> map;
   std::vector<long long> local;
   int pmin[3], pmax[3];
+  bool mf = false;     // matrix-free operators (op_mode 2, or auto)
 };
+
+bool mf_auto(const ga_desc* d);
 
 ga_status validate(const ga_desc* d, ga_ctx* ctx) {
   if (!d) { seterr(ctx, "desc is NULL"); return GA_ERR_ARG; }
@@ -130,6 +136,8 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
   if (!(d->pcg_refine_rtol >= 0.0) || d->pcg_refine_rtol >= 1.0) { seterr(ctx, "pcg_refine_rtol must be in [0,1)"); return GA_ERR_ARG; }
   if (!(d->pcg_rtol > 0.0) || d->pcg_maxit < 1) { seterr(ctx, "pcg_rtol > 0 and pcg_maxit >= 1 required"); return GA_ERR_ARG; }
   if (d->param_set != 0 && d->param_set != 1) { seterr(ctx, "param_set must be 0 or 1"); return GA_ERR_ARG; }
+  if (d->op_mode < 0 || d->op_mode > 2) { seterr(ctx, "op_mode must be 0, 1 or 2"); return GA_ERR_ARG; }
+  if (d->op_mode == 2 && d->npatch != 1) { seterr(ctx, "op_mode 2 (matrix-free) supports a single patch"); return GA_ERR_ARG; }
   double a[KMAX], b[KMAX], g[KMAX], f[KMAX], th;
   int rc = scheme_params(d->k, d->rho_b, d->rho_s, d->param_set, a, b, g, f, &th);
   if (rc != 0) { seterr(ctx, "invalid rho_b/rho_s (need 0 <= rho_s <= rho_b <= 1; param_set 1 needs rho < 1)"); return GA_ERR_PARAM; }
@@ -149,6 +157,7 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
 // Global masked grid, boxes, maps.
 ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_conformity) {
   sh.dim = d->dim; sh.nvec = d->ncomp; sh.p = d->p; sh.n = d->n; sh.m = d->n + d->p; sh.k = d->k; sh.W1 = 2 * d->p + 1;
+  sh.mf = d->op_mode == 2 || (d->op_mode == 0 && mf_auto(d));
   sh.S = (long long)sh.W1 * sh.W1 * (sh.dim == 3 ? sh.W1 : 1);
   const int m = sh.m, dim = sh.dim;
   int cmax[3] = {0, 0, 0};
@@ -261,6 +270,13 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
   return GA_OK;
 }
 
+// op_mode 0: which representation is faster, from the measured operator times
+// (DESIGN.md §6 "Stencil vs matrix-free"); multi-patch grids always use stencils.
+bool mf_auto(const ga_desc* d) {
+  if (d->npatch != 1) return false;
+  return d->dim == 3 && d->p >= 5;
+}
+
 size_t sweep_bytes(int n, int p) {
   // dinv + coef + H + A (L <= 6 levels, C <= 64 chunks)
   return align256(sizeof(double) * ((size_t)n * (1 + 2 * p) + (size_t)6 * 64 * p * p));
@@ -271,8 +287,17 @@ Layout make_layout(const Shape& sh) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
   const long long npts = sh.g.npts;
-  L.off_coefM = take(sizeof(double) * sh.S * sh.g.cs);
-  L.off_coefK = take(sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1));
+  const bool mfK = sh.mf && sh.nvec == 1;  // the elastic K stays a stencil
+  L.off_coefM = take(sh.mf ? 0 : sizeof(double) * sh.S * sh.g.cs);
+  L.off_coefK = take(mfK ? 0 : sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1));
+  {
+    const long long nq = (long long)sh.n * (sh.p + 1);
+    const long long nqd = sh.dim == 3 ? nq * nq * nq : nq * nq;
+    L.off_mfWM = take(sh.mf ? sizeof(double) * nqd : 0);
+    L.off_mfWK = take(mfK ? sizeof(double) * nqd * (sh.dim == 3 ? 6 : 3) : 0);
+    L.off_mftab = take(sh.mf ? sizeof(double) * 2 * nq * (sh.p + 1) : 0);
+    L.off_diag = take(sh.mf ? sizeof(double) * npts : 0);
+  }
   L.off_chain = take(sizeof(double) * 3 * sh.k * sh.nvec * sh.g.padded);
   for (int i = 0; i < 8; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
   const bool multi = sh.prec.size() > 1;
@@ -323,8 +348,8 @@ size_t asm_fixed_bytes(const Shape& sh) {
 }
 
 __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, int loz, const double* d0,
-                          const double* d1, const double* d2, const double* coefM, long long S, int nx, int ny,
-                          const unsigned char* mask) {
+                          const double* d1, const double* d2, const double* coefM, const double* diagM, long long S,
+                          int nx, int ny, const unsigned char* mask) {
   const long long nbox = (long long)bx * by * bz;
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nbox) return;
@@ -333,7 +358,8 @@ __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, i
   double v = 0.0;
   if (!mask || mask[gi]) {
     const double dh = d0[ix] * d1[iy] * (d2 ? d2[iz] : 1.0);
-    const double D = coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)];  // diag(M), blocked layout
+    // diag(M): matrix-free array, or the centre offset of the blocked stencil layout
+    const double D = diagM ? diagM[gi] : coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)];
     v = sqrt(dh / D);  // s = sqrt(Dh / D): calM^{-1} = S Mh^{-1} S
   }
   s[e] = v;
@@ -385,6 +411,11 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
   a.x = x; a.y = y; a.b = c->b;
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
+  if (c->mf && !a.elastic) {
+    a.mf = 1; a.mfstiff = which; a.mfn = c->n; a.mfj0 = 0;
+    a.mfW = which == 0 ? c->mfWM : c->mfWK; a.mfws = c->mfws;
+    a.mfv = c->mftv; a.mfd = c->mftd;
+  }
   a.mode = mode;
   // p = z + beta p as a separate elementwise pass (measured faster than forming
   // it on the SpMV input window, which doubles the vector loads)
@@ -562,12 +593,13 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   double* X2 = dim == 3 ? take(sizeof(double) * W1 * W1 * m * m * maxq) : nullptr;
   if (off > scratch_bytes) { seterr(ctx, "scratch too small (slab)"); return GA_ERR_OOM; }
 
-  CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.cs, s));
-  CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1), s));
+  const bool mfK = sh.mf && sh.nvec == 1;
+  if (!sh.mf) CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.cs, s));
+  if (!mfK) CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1), s));
   // term list: (target block pointer, spec, derivative flags per direction)
   struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; int ab; };
   std::vector<Term> terms;
-  {
+  if (!sh.mf) {
     Term t;
     memset(&t, 0, sizeof(t));
     t.coef = ctx->coefM;
@@ -575,7 +607,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
     t.ts.scale = sh.nvec == 3 ? ctx->d.density : 1.0;
     terms.push_back(t);
   }
-  if (sh.nvec == 1) {
+  if (sh.nvec == 1 && !mfK) {
     for (int c = 0; c < dim; ++c)
       for (int e = 0; e < dim; ++e) {
         Term t;
@@ -585,7 +617,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         for (int d = 0; d < 3; ++d) { t.sflag[d] = (d == c); t.tflag[d] = (d == e); }
         terms.push_back(t);
       }
-  } else {
+  } else if (sh.nvec == 3) {
     for (int a = 0; a < 3; ++a)
       for (int b = 0; b < 3; ++b)
         for (int c = 0; c < 3; ++c)
@@ -610,6 +642,26 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
       const int qa = ea * pp1, nqs = (eb - ea) * pp1;
       const long long npts_s = lowpts * nqs;
       launch_geometry(P, dim, qa, nqs, geo, npts_s, dmin, s);
+      if (sh.mf) {
+        // Gauss-point data of the matrix-free operators for quadrature planes [qa, qa + nqs)
+        // (overlapping slabs rewrite identical values): W_M = density w|J|, and for the scalar
+        // K the symmetric omega^2 w|J| (J^-1 J^-T)_{ce}, c <= e (SoA, stride mfws)
+        TermSpec tm;
+        memset(&tm, 0, sizeof(tm));
+        tm.kind = 0;
+        tm.scale = sh.nvec == 3 ? ctx->d.density : 1.0;
+        launch_wterm(geo, npts_s, npts_s, dim, tm, ctx->mfWM + (long long)qa * lowpts, s);
+        if (mfK) {
+          int idx = 0;
+          for (int c = 0; c < dim; ++c)
+            for (int e = c; e < dim; ++e, ++idx) {
+              TermSpec tk;
+              memset(&tk, 0, sizeof(tk));
+              tk.kind = 1; tk.c = c; tk.e = e; tk.scale = ctx->d.omega * ctx->d.omega;
+              launch_wterm(geo, npts_s, npts_s, dim, tk, ctx->mfWK + idx * ctx->mfws + (long long)qa * lowpts, s);
+            }
+        }
+      }
       for (const Term& t : terms) {
         launch_wterm(geo, npts_s, npts_s, dim, t.ts, W, s);
         const double* A0 = dA + (size_t)(t.sflag[0] * 2 + t.tflag[0]) * asz;
@@ -805,6 +857,16 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->ws = ws; ctx->ws_bytes = workspace_bytes;
   ctx->coefM = (double*)(ws + L.off_coefM);
   ctx->coefK = (double*)(ws + L.off_coefK);
+  ctx->mf = sh.mf;
+  if (sh.mf) {
+    const long long nq = (long long)sh.n * (sh.p + 1);
+    ctx->mfws = sh.dim == 3 ? nq * nq * nq : nq * nq;
+    ctx->mfWM = (double*)(ws + L.off_mfWM);
+    ctx->mfWK = sh.nvec == 1 ? (double*)(ws + L.off_mfWK) : nullptr;
+    ctx->mftv = (double*)(ws + L.off_mftab);
+    ctx->mftd = ctx->mftv + nq * (sh.p + 1);
+    ctx->diagM = (double*)(ws + L.off_diag);
+  }
   ctx->chain = (double*)(ws + L.off_chain);
   double** mv[8] = {&ctx->pred, &ctx->b, &ctx->x, &ctx->r, &ctx->z, &ctx->pv, &ctx->q, &ctx->pv1};
   for (int i = 0; i < 8; ++i) *mv[i] = (double*)(ws + L.off_mv[i]);
@@ -834,9 +896,18 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     CKD(cudaMemcpyAsync(ctx->mask, sh.mask.data(), sh.g.npts, cudaMemcpyHostToDevice, s));
     CKD(cudaMemcpyAsync(ctx->map, sh.map.data(), sizeof(long long) * sh.nfree, cudaMemcpyHostToDevice, s));
   }
+  if (sh.mf) {  // 1D basis tables of the matrix-free apply (host_math.cpp)
+    Tables1D T0 = make_tables(sh.p, sh.n);
+    CKD(cudaMemcpyAsync(ctx->mftv, T0.val.data(), sizeof(double) * T0.val.size(), cudaMemcpyHostToDevice, s));
+    CKD(cudaMemcpyAsync(ctx->mftd, T0.der.data(), sizeof(double) * T0.der.size(), cudaMemcpyHostToDevice, s));
+  }
   // assembly
   rc = assemble(ctx, sh, (char*)d_scratch, scratch_bytes, s);
   if (rc != GA_OK) { ga_destroy(ctx); return rc; }
+  if (sh.mf) {
+    launch_mf_diag(sh.g, sh.p, sh.n, ctx->mfWM, ctx->mftv, ctx->diagM, s);
+    CKD(cudaGetLastError());
+  }
   // preconditioner: per patch 1D factors (host) and scaling s (device)
   Tables1D T = make_tables(sh.p, sh.n);
   std::vector<double> band = param_mass_band(T);
@@ -885,7 +956,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     const double* center = ctx->coefM;  // blocked layout: k_scaling indexes offset S/2
     k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
                                                                  pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
-                                                                 center, ctx->S, sh.g.nx, sh.g.ny, ctx->mask);
+                                                                 center, ctx->diagM, ctx->S, sh.g.nx, sh.g.ny, ctx->mask);
     CKD(cudaGetLastError());
     CKD(cudaStreamSynchronize(s));  // tmp reused by the next patch
   }
@@ -899,7 +970,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     // latency-bound regime: little data per PCG phase (C2-like); bandwidth-bound grids keep the graph path
     const bool small = (long long)sh.g.npts * sh.k <= 600000 && (double)sh.S * sh.g.npts * 8.0 <= 64e6;
     const bool want = pe ? (*pe != '0') : small;
-    ctx->persist = want && persist_supported(persist_args(ctx));
+    ctx->persist = want && !ctx->mf && persist_supported(persist_args(ctx));
     const char* te = getenv("GA_TRACE");
     if (te && *te && *te != '0') {
       cudaMalloc(&ctx->trace, 8192 * sizeof(long long));  // debug only
@@ -1161,6 +1232,7 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
 }
 
 int ga_uses_persistent_solver(const ga_ctx* ctx) { return ctx && ctx->persist ? 1 : 0; }
+int ga_uses_matrix_free(const ga_ctx* ctx) { return ctx && ctx->mf ? 1 : 0; }
 
 // debug: copy the persistent-solver trace (GA_TRACE=1) to the host; returns slots copied
 int ga_debug_trace(ga_ctx* ctx, long long* host, int n) {

@@ -32,8 +32,25 @@ struct SpmvArgs {
   DevStatus* st;
   double* partial;
   unsigned int* counter;
+  // matrix-free sum-factorised operator (mf = 1; coef unused), single patch, scalar M / K
+  // or the elastic mass (density * scalar M per component), DESIGN.md "Matrix-free operator"
+  int mf;              // 1: apply by sum factorisation from the quadrature data
+  int mfstiff;         // 0: mass  sum_q W B_i B_j ;  1: stiffness sum_q grad^T B_i W grad B_j
+  int mfn;             // elements per direction
+  int mfj0;            // first right-hand side of this launch (sub-batches of <= 2 rhs)
+  const double* mfW;   // mass: W[nq^d]; stiffness: d(d+1)/2 symmetric entries, SoA with stride mfws
+  long long mfws;      // nq^d, nq = n (p+1) (global tensor Gauss grid, x fastest)
+  const double* mfv;   // 1D basis values  [nq][p+1]  (local function a of element q/(p+1))
+  const double* mfd;   // 1D derivatives   [nq][p+1]
 };
 void launch_spmv(const SpmvArgs& a, cudaStream_t s);
+// matrix-free variants (matfree.cu): the same contract as launch_spmv for a.mf = 1
+void launch_matfree(const SpmvArgs& a, cudaStream_t s);
+// fixed-order sum of nb block partials + the PCG scalar step (SPMV_PQ / SPMV_TRUERES)
+void launch_spmv_fin(const SpmvArgs& a, unsigned int nb, cudaStream_t s);
+// diag(M) of the matrix-free mass operator on the single-patch grid, diag[npts]
+void launch_mf_diag(const GridDesc& g, int p, int n, const double* W, const double* tv, double* diag,
+                    cudaStream_t s);
 
 struct PrecArgs {
   GridDesc g;

@@ -129,7 +129,20 @@ static void spmv_p(const SpmvArgs& a, cudaStream_t s) {
   if (a.nvec == 3) spmv_nc<P, 3>(a, s);
   else spmv_nc<P, 1>(a, s);
 }
+void launch_spmv_fin(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
+  switch (a.kk) {
+    case 1: k_spmv_fin<1><<<1, 1024, 0, s>>>(a, nb); break;
+    case 2: k_spmv_fin<2><<<1, 1024, 0, s>>>(a, nb); break;
+    case 3: k_spmv_fin<3><<<1, 1024, 0, s>>>(a, nb); break;
+    default: k_spmv_fin<4><<<1, 1024, 0, s>>>(a, nb); break;
+  }
+}
+
 void launch_spmv(const SpmvArgs& a, cudaStream_t s) {
+  if (a.mf) {
+    launch_matfree(a, s);
+    return;
+  }
   switch (a.p) {
     case 1: spmv_p<1>(a, s); break;
     case 2: spmv_p<2>(a, s); break;

@@ -24,7 +24,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
 
 EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
-            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_destroy",
+            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_destroy",
             "ga_last_error"]
 
 
@@ -38,7 +38,7 @@ class ga_desc(ctypes.Structure):
                 ("lame_mu", c_double), ("density", c_double), ("k", c_int), ("rho_b", c_double),
                 ("rho_s", c_double), ("param_set", c_int), ("dt", c_double), ("pcg_rtol", c_double),
                 ("pcg_maxit", c_int), ("pcg_refine", c_int), ("pcg_refine_rtol", c_double),
-                ("unstable_factor", c_double)]
+                ("unstable_factor", c_double), ("op_mode", c_int)]
 
 
 class ga_stats(ctypes.Structure):
@@ -76,6 +76,7 @@ def _load():
         "ga_free_dof_map": (c_int, [c_void_p, POINTER(c_longlong)]),
         "ga_profile_op": (c_int, [c_void_p, c_int, c_int, c_void_p]),
         "ga_uses_persistent_solver": (c_int, [c_void_p]),
+        "ga_uses_matrix_free": (c_int, [c_void_p]),
         "ga_destroy": (None, [c_void_p]),
         "ga_last_error": (ctypes.c_char_p, [c_void_p]),
     }
@@ -109,7 +110,7 @@ def ga_params(k, rho_b, rho_s=None, param_set=0):
 
 def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3, param_set=0,
               omega=1.0, lam=1.0, mu=1.0, density=1.0, pcg_rtol=1e-13, pcg_maxit=500,
-              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6):
+              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6, op_mode=0):
     """ga_desc from [(cell, ctrl ndarray (m^dim, dim))].  Keeps the ctrl arrays
     alive on the returned object (`_keep`)."""
     arr = (ga_patch * len(patches))()
@@ -127,7 +128,7 @@ def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3,
                 # refinement restart (R8): needed where kappa(M) ~1e7-1e8 (3D p >= 5)
                 pcg_refine=(1 if p >= 5 else 0) if pcg_refine is None else pcg_refine,
                 pcg_refine_rtol=(1e-3 if p >= 5 else 0.0) if pcg_refine_rtol is None else pcg_refine_rtol,
-                unstable_factor=unstable_factor)
+                unstable_factor=unstable_factor, op_mode=op_mode)
     d._keep = (arr, keep)
     return d
 
@@ -225,6 +226,9 @@ class Context:
 
     def persistent(self):
         return bool(lib.ga_uses_persistent_solver(self.ctx))
+
+    def matrix_free(self):
+        return bool(lib.ga_uses_matrix_free(self.ctx))
 
     def free_dof_map(self):
         ncomp = self.desc.ncomp

@@ -1,0 +1,129 @@
+"""GPU parity of the matrix-free operator (op_mode 2): the
+sum-factorised apply of M and K against the oracle's assembled matrices
+element by element, against the library's own stencil path, and the mass
+solve / trajectories with it against the oracle (relative M-norm bar of
+BASELINE.json).  Cases span several x/y tiles with ragged tails (3D tiles are
+8 x 8 bases, 2D tiles 128), z/y chunking, every degree 1..7 in 3D, the
+elastic mass, and k = 1..4 right-hand sides (sub-batches of 2)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import integrator
+
+from _helpers import Case, mnorm_rel, oracle_with_floor
+
+pytestmark = pytest.mark.gpu
+
+MF_CASES = {
+    "2d_p1_n9": synth.config("c2", p=1, n=9),
+    "2d_p2_identity": synth.config("c1", n=8),
+    "2d_p3_n10": synth.config("c2", n=10),
+    "2d_p3_n140_two_tiles": synth.config("c2", n=140),  # 141 free per direction: tiles of 128 + 13
+    "2d_p5_n7": synth.config("c2", p=5, n=7),
+    "3d_p1_n6": synth.config("c3", p=1, n=6),
+    "3d_p2_n11_ragged": synth.config("c3", p=2, n=11),  # 11 free per direction: tiles 8 + 3
+    "3d_p3_n5": synth.config("c3", p=3, n=5),
+    "3d_p4_n6": synth.config("c3", p=4, n=6),
+    "3d_p5_n3": synth.config("c3", p=5, n=3),
+    "3d_p6_n3": synth.config("c3", p=6, n=3),
+    "3d_p7_n2": synth.config("c3", p=7, n=2),
+    "3d_p3_n14_k3": synth.config("c3", p=3, n=14, k=3),  # 2 x 2 tiles, z chunks, rhs 2 + 1
+    "elastic_p2_n3": synth.config("c4", p=2, n=3),
+}
+
+
+@pytest.fixture(scope="module", params=sorted(MF_CASES))
+def mfcase(request):
+    c = Case(MF_CASES[request.param], op_mode=2)
+    assert c.ctx.matrix_free()
+    return c
+
+
+def test_mf_operators_elementwise(mfcase):
+    d = mfcase.disc
+    rng = np.random.default_rng(17)
+    for which, A in (("M", d.M), ("K", d.K)):
+        x = rng.standard_normal(A.shape[0])
+        y = mfcase.from_lib(mfcase.ctx.apply(which, mfcase.to_lib(x)))
+        ref = A @ x
+        # sum-factorised evaluation = the same quadrature sums in another order
+        # K's quadrature terms cancel (constants lie in its kernel), so its rounding is
+        # measured against |K||x| with a wider factor than M's
+        scale = (abs(A) @ np.abs(x)).max()
+        err = np.abs(y - ref).max()
+        assert err <= (2e-14 if which == "M" else 1e-13) * scale * max(1, d.p), (which, err / scale)
+    for col in [0, d.M.shape[0] // 3, d.M.shape[0] - 1]:
+        e = np.zeros(d.M.shape[0]); e[col] = 1.0
+        y = mfcase.from_lib(mfcase.ctx.apply("M", mfcase.to_lib(e)))
+        ref = d.M[:, col].toarray().ravel()
+        assert np.abs(y - ref).max() <= 1e-14 * abs(d.M[col, col]) * max(1, d.p)
+
+
+def test_mf_preconditioner_diag(mfcase):
+    # the scaling uses diag(M) computed matrix-free: calM^{-1} must equal the oracle's
+    from oracle import precond
+    P = precond.SchwarzPreconditioner(mfcase.disc)
+    x = np.random.default_rng(18).standard_normal(mfcase.disc.M.shape[0])
+    y = mfcase.from_lib(mfcase.ctx.apply("Pinv", mfcase.to_lib(x)))
+    ref = P(x)
+    assert np.abs(y - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+def test_mf_mass_solve(mfcase):
+    d = mfcase.disc
+    b = d.K @ mfcase.u0()
+    x, its = mfcase.ctx.solve_mass(mfcase.to_lib(b))
+    x = mfcase.from_lib(x)
+    ref = integrator.DirectMassSolver(d.M)(b)
+    # kappa(M) ~1e8..1e10 at 3D p = 6, 7: the bar includes the floor F of the
+    # same solve with M assembled by the same definitions, Gauss points in reverse order
+    from oracle import assembly
+    d2 = assembly.Discretization(mfcase.prob["patches"], d.p, d.n, d.dim, ncomp=d.ncomp, reverse_points=True)
+    floor = mnorm_rel(d.M, integrator.DirectMassSolver(d2.M)(b), ref)
+    err = mnorm_rel(d.M, x, ref)
+    assert err < max(1e-12 if d.p <= 4 else 2e-11, 10 * floor), (err, floor)
+    if mfcase.cfg["noise"] == 0.0:
+        assert its == 1
+
+
+@pytest.mark.parametrize("name", ["2d_p3_n10", "3d_p3_n5", "3d_p2_n11_ragged"])
+def test_mf_equals_stencil(name):
+    a = Case(MF_CASES[name], op_mode=1)
+    b = Case(MF_CASES[name], op_mode=2)
+    assert not a.ctx.matrix_free() and b.ctx.matrix_free()
+    x = np.random.default_rng(19).standard_normal(a.disc.nfree)
+    for which in ("M", "K"):
+        ya = a.from_lib(a.ctx.apply(which, a.to_lib(x)))
+        yb = b.from_lib(b.ctx.apply(which, b.to_lib(x)))
+        assert np.abs(ya - yb).max() <= 1e-13 * np.abs(ya).max(), which
+
+
+@pytest.mark.parametrize("cfg,nsteps", [
+    (synth.config("c2", n=24), 60),
+    (synth.config("c3", p=2, n=9, k=2, rho=0.5), 30),
+    (synth.config("c3", p=4, n=4, k=3, rho=0.0), 20),
+    (synth.config("c3", p=6, n=3, k=2, rho=0.0), 20),
+    (synth.config("c4", p=2, n=3), 15),
+    (synth.config("c2", n=8, k=4, rho=0.5), 20),
+])
+def test_mf_trajectory(cfg, nsteps):
+    c = Case(cfg, op_mode=2)
+    assert c.ctx.matrix_free()
+    d = c.disc
+    u0 = c.u0()
+    c.ctx.set_state(c.to_lib(u0))
+    c.ctx.advance(nsteps)
+    st = c.ctx.stats()
+    assert st.status == 0 and st.steps == nsteps
+    u, v, a = (c.from_lib(t) for t in c.ctx.get_state())
+    ref, floor = oracle_with_floor(d, cfg["k"], cfg["rho"], c.dt, u0, np.zeros_like(u0), nsteps, case=c)
+    errs = [mnorm_rel(d.M, x, y) for x, y in zip((u, v, a), ref[:3])]
+    assert all(e < max(1e-10, 10 * f) for e, f in zip(errs, floor)), (errs, floor)
+
+
+def test_mf_multipatch_rejected():
+    from paper_2102_11536_b200 import GAError
+    with pytest.raises(GAError) as ei:
+        Case(synth.config("c5", p=2, n=4), op_mode=2)
+    assert ei.value.code == -1
