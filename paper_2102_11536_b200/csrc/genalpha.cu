@@ -272,9 +272,15 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
 
 // op_mode 0: which representation is faster, from the measured operator times
 // (DESIGN.md §6 "Stencil vs matrix-free"); multi-patch grids always use stencils.
+// Measured (profiles/r01_matfree.md): the stencil SpMV at 0.8-0.97 of HBM bandwidth beats
+// the fp64-bound sum factorisation at every degree where the stencils fit, so op_mode 0
+// takes matrix-free only when the assembled M and K would not fit in the B200's HBM.
 bool mf_auto(const ga_desc* d) {
   if (d->npatch != 1) return false;
-  return d->dim == 3 && d->p >= 5;
+  const double W1 = 2.0 * d->p + 1.0, S = d->dim == 3 ? W1 * W1 * W1 : W1 * W1;
+  const double npts = std::pow((double)(d->n + d->p - 2), d->dim);
+  const double stencil_bytes = 8.0 * S * npts * (d->ncomp == 3 ? 10.0 : 2.0);
+  return stencil_bytes > 150e9;
 }
 
 size_t sweep_bytes(int n, int p) {

@@ -39,7 +39,9 @@ struct Mf3Shape {
   static constexpr int V = NF * VS;
   static constexpr int ACCS = DY * DX * KK;
   static constexpr int ACC = P1 * ACCS;
-  static constexpr int TOTAL = RING + TZ + TX + V + ACC;
+  static constexpr int TABX = EX * P1 * P1, TABY = EY * P1 * P1;  // per-tile 1D tables (val; der)
+  static constexpr int TAB = (STIFF ? 2 : 1) * (TABX + TABY);
+  static constexpr int TOTAL = RING + TZ + TX + V + ACC + TAB;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
 };
 
@@ -101,6 +103,10 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
   double* tx = tz + L::TZ;     // [NF][IY][QX][KK]   + x-contracted (N_x N_z; D_x N_z; N_x D_z)
   double* vv = tx + L::TX;     // [NF][DY][QX][KK]   after y forward, W, y back (owned y bases)
   double* acc = vv + L::V;     // [P1][DY][DX][KK]   output ring (slot = basis % P1)
+  double* snx = acc + L::ACC;  // [EX][P1][P1] N_x of the tile's elements (0 outside the patch)
+  double* sny = snx + L::TABX; // [EY][P1][P1]
+  double* sdx = sny + L::TABY; // derivatives (stiffness only)
+  double* sdy = sdx + L::TABX;
   const GridDesc g = a.g;
   const int n = a.mfn, m = n + P;
   const long long nq = (long long)n * P1;
@@ -120,6 +126,18 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
 #pragma unroll
   for (int j = 0; j < KK; ++j) dots[j] = 0.0;
   for (int i = tid; i < L::ACC; i += NT) acc[i] = 0.0;
+  for (int i = tid; i < L::TABX; i += NT) {
+    const int ex = exb + i / (P1 * P1);
+    const bool ok = ex >= 0 && ex < n;
+    snx[i] = ok ? __ldg(tv + (long long)exb * P1 * P1 + i) : 0.0;
+    if (STIFF) sdx[i] = ok ? __ldg(td + (long long)exb * P1 * P1 + i) : 0.0;
+  }
+  for (int i = tid; i < L::TABY; i += NT) {
+    const int ey = eyb + i / (P1 * P1);
+    const bool ok = ey >= 0 && ey < n;
+    sny[i] = ok ? __ldg(tv + (long long)eyb * P1 * P1 + i) : 0.0;
+    if (STIFF) sdy[i] = ok ? __ldg(td + (long long)eyb * P1 * P1 + i) : 0.0;
+  }
 
   constexpr int LPT = (PLANE + NT - 1) / NT;
   auto load_plane = [&](int bz, double (&pf)[LPT]) {
@@ -196,18 +214,18 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
       // (b) x contraction to the x Gauss points of the tile's elements
       for (int i = tid; i < L::TXS; i += NT) {
         const int j = i % KK, qxl = (i / KK) % QX, yl = i / (KK * QX);
-        const int exl = qxl / P1, qx = qxl - exl * P1, ex = exb + exl;
+        const int exl = qxl / P1;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-        if (ex >= 0 && ex < n) {
-          const double* nr = tv + ((long long)ex * P1 + qx) * P1;
-          const double* dr = td + ((long long)ex * P1 + qx) * P1;
+        {
+          const double* nr = snx + qxl * P1;  // zero rows outside the patch
+          const double* dr = sdx + qxl * P1;
           const double* t0 = tz + (yl * IX + exl) * KK + j;
 #pragma unroll
           for (int u = 0; u < P1; ++u) {
-            const double nxu = __ldg(nr + u);
+            const double nxu = nr[u];
             s0 = fma(nxu, t0[u * KK], s0);
             if (STIFF) {
-              s1 = fma(__ldg(dr + u), t0[u * KK], s1);
+              s1 = fma(dr[u], t0[u * KK], s1);
               s2 = fma(nxu, t0[PLANE + u * KK], s2);
             }
           }
@@ -216,13 +234,29 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
         if (STIFF) { tx[L::TXS + i] = s1; tx[2 * L::TXS + i] = s2; }
       }
       __syncthreads();
-      // (c) per (x Gauss point, rhs): walk the y elements
+      // (c) per (x Gauss point, rhs): walk the y elements; the quadrature data of the
+      //     next element is loaded one step ahead (software pipeline)
       for (int t = tid; t < QX * KK; t += NT) {
         const int j = t % KK, qxl = t / KK;
         const int ex = exb + qxl / P1;
         const bool xv = ex >= 0 && ex < n;
         const double* wbase = a.mfW + (qzg * nq) * nq + ((long long)exb * P1 + qxl);  // + qyg * nq
-        double in0[P1], in1[P1], in2[P1], ac0[P1], ac1[P1], ac2[P1];
+        constexpr int NW = STIFF ? 6 * P1 : P1;
+        double in0[P1], in1[P1], in2[P1], ac0[P1], ac1[P1], ac2[P1], wn[NW];
+        auto load_w = [&](int eyl) {
+          const int ey = eyb + eyl;
+          const bool ok = xv && ey >= 0 && ey < n;
+          const double* wr = wbase + (long long)ey * P1 * nq;
+#pragma unroll
+          for (int qy = 0; qy < P1; ++qy) {
+            if (!STIFF) {
+              wn[qy] = ok ? __ldg(wr + qy * nq) : 0.0;
+            } else {
+#pragma unroll
+              for (int c = 0; c < 6; ++c) wn[c * P1 + qy] = ok ? __ldg(wr + qy * nq + c * a.mfws) : 0.0;
+            }
+          }
+        };
 #pragma unroll
         for (int u = 0; u < P; ++u) {
           in0[u] = tx[(u * QX + qxl) * KK + j];
@@ -233,61 +267,53 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
         }
 #pragma unroll
         for (int u = 0; u < P1; ++u) { ac0[u] = 0.0; ac1[u] = 0.0; ac2[u] = 0.0; }
+        if (!STIFF) load_w(0);
         for (int eyl = 0; eyl < EY; ++eyl) {
           in0[P] = tx[((eyl + P) * QX + qxl) * KK + j];
           if (STIFF) {
             in1[P] = tx[L::TXS + ((eyl + P) * QX + qxl) * KK + j];
             in2[P] = tx[2 * L::TXS + ((eyl + P) * QX + qxl) * KK + j];
           }
-          const int ey = eyb + eyl;
-          if (xv && ey >= 0 && ey < n) {
-            const double* wr = wbase + (long long)ey * P1 * nq;
-            double w[STIFF ? 6 * P1 : P1];
+          double w[NW];
+          if constexpr (STIFF) load_w(eyl);  // 6 (p+1) values: no room to pipeline in registers
 #pragma unroll
-            for (int qy = 0; qy < P1; ++qy) {
-              if (!STIFF) {
-                w[qy] = __ldg(wr + qy * nq);
-              } else {
+          for (int c = 0; c < NW; ++c) w[c] = wn[c];
+          if (!STIFF && eyl + 1 < EY) load_w(eyl + 1);
 #pragma unroll
-                for (int c = 0; c < 6; ++c) w[c * P1 + qy] = __ldg(wr + qy * nq + c * a.mfws);
+          for (int qy = 0; qy < P1; ++qy) {
+            const double* nr = sny + (eyl * P1 + qy) * P1;  // zero outside the patch
+            double ny[P1];
+#pragma unroll
+            for (int u = 0; u < P1; ++u) ny[u] = nr[u];
+            if (!STIFF) {
+              double s = 0.0;
+#pragma unroll
+              for (int u = 0; u < P1; ++u) s = fma(ny[u], in0[u], s);
+              s *= w[qy];
+#pragma unroll
+              for (int u = 0; u < P1; ++u) ac0[u] = fma(ny[u], s, ac0[u]);
+            } else {
+              const double* dr = sdy + (eyl * P1 + qy) * P1;
+              double dy[P1];
+#pragma unroll
+              for (int u = 0; u < P1; ++u) dy[u] = dr[u];
+              double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+              for (int u = 0; u < P1; ++u) {
+                gx = fma(ny[u], in1[u], gx);  // D_x N_y N_z
+                gy = fma(dy[u], in0[u], gy);  // N_x D_y N_z
+                gz = fma(ny[u], in2[u], gz);  // N_x N_y D_z
               }
-            }
+              const double w00 = w[qy], w01 = w[P1 + qy], w02 = w[2 * P1 + qy];
+              const double w11 = w[3 * P1 + qy], w12 = w[4 * P1 + qy], w22 = w[5 * P1 + qy];
+              const double fx = w00 * gx + w01 * gy + w02 * gz;
+              const double fy = w01 * gx + w11 * gy + w12 * gz;
+              const double fz = w02 * gx + w12 * gy + w22 * gz;
 #pragma unroll
-            for (int qy = 0; qy < P1; ++qy) {
-              const double* nr = tv + ((long long)ey * P1 + qy) * P1;
-              double ny[P1];
-#pragma unroll
-              for (int u = 0; u < P1; ++u) ny[u] = __ldg(nr + u);
-              if (!STIFF) {
-                double s = 0.0;
-#pragma unroll
-                for (int u = 0; u < P1; ++u) s = fma(ny[u], in0[u], s);
-                s *= w[qy];
-#pragma unroll
-                for (int u = 0; u < P1; ++u) ac0[u] = fma(ny[u], s, ac0[u]);
-              } else {
-                const double* dr = td + ((long long)ey * P1 + qy) * P1;
-                double dy[P1];
-#pragma unroll
-                for (int u = 0; u < P1; ++u) dy[u] = __ldg(dr + u);
-                double gx = 0.0, gy = 0.0, gz = 0.0;
-#pragma unroll
-                for (int u = 0; u < P1; ++u) {
-                  gx = fma(ny[u], in1[u], gx);  // D_x N_y N_z
-                  gy = fma(dy[u], in0[u], gy);  // N_x D_y N_z
-                  gz = fma(ny[u], in2[u], gz);  // N_x N_y D_z
-                }
-                const double w00 = w[qy], w01 = w[P1 + qy], w02 = w[2 * P1 + qy];
-                const double w11 = w[3 * P1 + qy], w12 = w[4 * P1 + qy], w22 = w[5 * P1 + qy];
-                const double fx = w00 * gx + w01 * gy + w02 * gz;
-                const double fy = w01 * gx + w11 * gy + w12 * gz;
-                const double fz = w02 * gx + w12 * gy + w22 * gz;
-#pragma unroll
-                for (int u = 0; u < P1; ++u) {
-                  ac0[u] = fma(ny[u], fx, ac0[u]);
-                  ac1[u] = fma(dy[u], fy, ac1[u]);
-                  ac2[u] = fma(ny[u], fz, ac2[u]);
-                }
+              for (int u = 0; u < P1; ++u) {
+                ac0[u] = fma(ny[u], fx, ac0[u]);
+                ac1[u] = fma(dy[u], fy, ac1[u]);
+                ac2[u] = fma(ny[u], fz, ac2[u]);
               }
             }
           }
@@ -315,18 +341,17 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
         double r0 = 0.0, r1 = 0.0;
 #pragma unroll
         for (int e2 = 0; e2 <= P; ++e2) {
-          const int exl = bxl + e2, ex = exb + exl;
-          if (ex < 0 || ex >= n) continue;
-          const int u = P - e2;  // local index of basis bx within element ex
+          const int exl = bxl + e2;
+          const int u = P - e2;  // local index of basis bx within element exl (zero rows outside)
           const double* vr = vv + (byl * QX + exl * P1) * KK + j;
 #pragma unroll
           for (int qx = 0; qx < P1; ++qx) {
-            const long long row = ((long long)ex * P1 + qx) * P1 + u;
-            const double nxv = __ldg(tv + row);
+            const int row = (exl * P1 + qx) * P1 + u;
+            const double nxv = snx[row];
             if (!STIFF) {
               r0 = fma(nxv, vr[qx * KK], r0);
             } else {
-              r0 = fma(__ldg(td + row), vr[qx * KK], r0);
+              r0 = fma(sdx[row], vr[qx * KK], r0);
               r0 = fma(nxv, vr[L::VS + qx * KK], r0);
               r1 = fma(nxv, vr[2 * L::VS + qx * KK], r1);
             }

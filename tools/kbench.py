@@ -14,6 +14,7 @@ from paper_2102_11536_b200 import Context, ga_params, make_desc
 
 args = dict(a.split("=") for a in sys.argv[2:])
 reps = int(args.pop("reps", 50))
+op_mode = int(args.pop("op", 0))
 cfg = synth.config(sys.argv[1] if len(sys.argv) > 1 else "c2", **{k: (float(v) if "." in v else int(v)) for k, v in args.items()})
 prob = synth.make_problem(cfg)
 nc = cfg.get("ncomp", 1)
@@ -21,7 +22,7 @@ _, _, _, _, th = ga_params(cfg["k"], cfg["rho"])
 cp = {1: 12.0, 2: 10.0, 3: 14.56, 4: 24.49, 5: 39.3, 6: 59.5, 7: 88.0}[cfg["p"]]
 lam = 1.2 * cfg["dim"] * cp * cfg["n"] ** 2 * (1.73 if nc > 1 else 1.0)
 dt = cfg["cfl_frac"] * math.sqrt(th / lam)
-desc = make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, k=cfg["k"], rho=cfg["rho"], dt=dt)
+desc = make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, k=cfg["k"], rho=cfg["rho"], dt=dt, op_mode=op_mode)
 ctx = Context(desc)
 fmap = ctx.free_dof_map()
 m = cfg["n"] + cfg["p"]
@@ -49,7 +50,7 @@ def timed(fn, n, cold):
 
 
 names = ["spmv_M(PQ)", "spmv_K(NEGB)", "precond", "predict", "spmv_M(APPLY)", "p_update"]
-print(f"config {cfg['name']} p={cfg['p']} n={cfg['n']} k={cfg['k']} N={ctx.n_free}")
+print(f"config {cfg['name']} p={cfg['p']} n={cfg['n']} k={cfg['k']} N={ctx.n_free} matrix_free={ctx.matrix_free()}")
 for op in range(6):
     warm_batch = timed(lambda: ctx.profile_op(op, reps), 3, False) / reps
     cold = timed(lambda: ctx.profile_op(op, 1), 10, True)
