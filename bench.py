@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--rho", type=float)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--lam-iters", type=int, default=60, help="power iterations for lambda_max (dt)")
+    ap.add_argument("--op-mode", type=int, default=0, choices=[0, 1, 2],
+                    help="0 auto (measured-faster / capacity), 1 stencil, 2 matrix-free")
     return ap.parse_args()
 
 
@@ -201,6 +204,30 @@ def algorithmic_bytes(op, ctx_info):
     return 8 * nv * N * (3 * k + k)
 
 
+# B200 fp64: 148 SMs x 64 DFMA/clk/SM x 2 flop x 1.965 GHz (sm_max_mhz) = 37.2 TFLOP/s
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def matfree_flops(op, cfg, nf):
+    """Algorithmic flops of one matrix-free apply (op 0 = M, op 1 = scalar K) over the k
+    right-hand sides: the non-redundant global sum factorisation,
+    forward contractions z, x, y (free bases -> Gauss points), the pointwise W product and
+    the mirrored backward contractions; 2 flops per FMA."""
+    p, n, d, k = cfg["p"], cfg["n"], cfg["dim"], cfg["k"]
+    q = n * (p + 1)
+    if d == 3:
+        stages = [nf * nf * q, nf * q * q, q * q * q]
+    else:
+        stages = [nf * q, q * q]
+    if op == 0:
+        fwd = sum(stages) * (p + 1)
+        return k * (2 * 2 * fwd + q ** d) * cfg.get("ncomp", 1)
+    fields = [2, 3, 3] if d == 3 else [2, 2]
+    fwd = sum(f * st for f, st in zip(fields, stages)) * (p + 1)
+    wprod = (d * d) * 2 * q ** d
+    return k * (2 * 2 * fwd + wprod)
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -217,13 +244,13 @@ def run_ours(args, rank, world, local_rank):
     _, _, _, _, thmax = ga_params(cfg["k"], cfg["rho"])
     # dt from the GPU's own lambda_max estimate (power iteration through the library)
     probe = Context(make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, k=cfg["k"], rho=cfg["rho"],
-                              dt=1e-6, **mat), device=dev)
-    lam = probe.lambda_max(60)
+                              dt=1e-6, op_mode=args.op_mode, **mat), device=dev)
+    lam = probe.lambda_max(args.lam_iters)
     probe.close()
     del probe
     dt = cfg["cfl_frac"] * math.sqrt(thmax / lam)
     desc = make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], ncomp=nc, k=cfg["k"], rho=cfg["rho"], dt=dt,
-                     **mat)
+                     op_mode=args.op_mode, **mat)
     ctx = Context(desc, device=dev)
     stream = ctx.stream
     fmap = ctx.free_dof_map()
@@ -278,6 +305,11 @@ def run_ours(args, rank, world, local_rank):
     names = {0: "k_spmv_sm(M)+p.q", 1: "k_spmv_sm(K)", 2: "preconditioner (k_line_tile x d, fused scaling/update/dots)",
              3: "k_stage(predictor pass)", 5: "k_p_update"}
     persistent = ctx.persistent()
+    mfree = ctx.matrix_free()
+    if mfree:
+        names[0] = "k_mf3/k_mf2(M, matrix-free)+p.q"
+        if nc == 1:
+            names[1] = "k_mf3/k_mf2(K, matrix-free)"
     ops = [0, 1, 2, 3, 5] + ([6] if persistent else [])
     steps = args.steps
     L = loop_iters / steps  # lock-stepped PCG iterations per step (one solve set per step)
@@ -299,6 +331,13 @@ def run_ours(args, rank, world, local_rank):
             durs.append(e0.elapsed_time(e1))
         avg = sum(durs) / len(durs)
         kern[op] = dict(name=names[op], ms=avg, bytes=info_bytes[op])
+        if mfree and (op == 0 or (op == 1 and nc == 1)):
+            nfd = G[0]  # free bases per direction (single patch)
+            qd = cfg["n"] * (cfg["p"] + 1)
+            # compulsory bytes: Gauss-point data once (1 or d(d+1)/2 values), read x, write y
+            kern[op]["bytes"] = 8 * qd ** cfg["dim"] * (1 if op == 0 else cfg["dim"] * (cfg["dim"] + 1) // 2) + \
+                16 * nc * cfg["k"] * info["npts"]
+            kern[op]["flops"] = matfree_flops(op, cfg, nfd)
     if persistent:
         per_step_launches = {0: 0.0, 1: 1.0, 2: 0.0, 3: 1.0, 5: 0.0, 6: 1.0}
     else:
@@ -309,6 +348,7 @@ def run_ours(args, rank, world, local_rank):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = kern[dom]["bytes"] / (kern[dom]["ms"] * 1e-3) / 1e9
+    alu = "flops" in kern[dom]
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -329,6 +369,15 @@ def run_ours(args, rank, world, local_rank):
                 "note": ("persistent solver: the whole lock-stepped solve is one launch; its 'achieved' counts the "
                          "algorithmic bytes of all its SpMVs, preconditioner applications and updates" if persistent
                          else "separate kernels per PCG phase inside a CUDA graph")}
+    if alu:  # matrix-free operator: fp64-ALU bound
+        tf = kern[dom]["flops"] / (kern[dom]["ms"] * 1e-3) / 1e12
+        roofline.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": tf / FP64_PEAK_TFLOPS, "algorithmic_flops": kern[dom]["flops"],
+                         "hbm_GB/s": achieved,
+                         "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)"})
+    for o in kern:
+        if "flops" in kern[o]:
+            roofline["kernels"][kern[o]["name"]]["TFLOP/s"] = kern[o]["flops"] / kern[o]["ms"] / 1e9
 
     # ---- end to end through the public API with host buffers
     u0_host = torch.tensor(u0_np, dtype=torch.float64).pin_memory()
@@ -363,7 +412,8 @@ def run_ours(args, rank, world, local_rank):
                            "lockstep_iters_per_step": loop_iters / steps,
                            "l2": "flushed between timed steps (256 MiB write), working set "
                                  f"{ctx.workspace.numel() / 2**20:.0f} MiB",
-                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                           "operators": "matrix-free" if mfree else "stencil"},
                 "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")}}
         if world == 1 and not args.no_cpu_baseline:

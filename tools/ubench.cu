@@ -15,6 +15,21 @@ __global__ void k_dfma(double* out, long long* cyc, int n) {
   if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+// fp64 FMA throughput: 8 independent chains per thread, many warps per SM
+__global__ void k_dfma_tput(double* out, int n) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+  const double b = 1.0000001, c = 1e-9;
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = fma(a[j], b, c);
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  if (s == 1.2345) out[threadIdx.x] = s;
+}
+
 __global__ void k_lds(double* out, long long* cyc, int n) {
   __shared__ int nxt[1024];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) nxt[i] = (i * 97 + 13) & 1023;
@@ -163,6 +178,21 @@ int main() {
     cudaDeviceSynchronize();
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("grid.sync (%d blocks x 256)    %8.1f cycles\n", nsm * b, (double)h / nn);
+  }
+
+  {  // fp64 FMA throughput (device-wide, CUDA events)
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    const int iters = 20000, blocks = nsm * 8, threads = 256;
+    k_dfma_tput<<<blocks, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    k_dfma_tput<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8 * iters * (double)blocks * threads;
+    printf("fp64 FMA throughput             %8.2f TFLOP/s (%d SMs)\n", flops / (ms * 1e-3) / 1e12, nsm);
   }
 
   unsigned int* cnt;
