@@ -610,10 +610,10 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
   const bool single = (a.npatch == 1 && a.t[0] == nullptr);
   // line mode: tiles (chunked, shared memory; needed when lines are few, 2D)
   // or streaming thread-per-line sweeps (many lines, 3D).  GA_LINE_MODE overrides.
-  static int line_mode = -1;  // 0 auto, 1 tile, 2 stream
+  static int line_mode = -1;  // 0 auto, 1 tile, 2 stream, 3 slab
   if (line_mode < 0) {
     const char* e = getenv("GA_LINE_MODE");
-    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : 0);
+    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : ((e && e[0] == 'b') ? 3 : 0));
   }
   long long minslots = 1LL << 62;
   for (int pr = 0; pr < a.npatch; ++pr)
@@ -623,7 +623,9 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
         if (e2 != d) sl *= a.bd[pr][e2];
       minslots = std::min(minslots, sl);
     }
-  const bool stream = line_mode == 2 || (line_mode == 0 && minslots >= 148LL * 128);
+  const bool stream = line_mode >= 2 || (line_mode == 0 && minslots >= 148LL * 128);
+  // many-line 3D grids: shared-memory slab sweeps (forward + backward on-chip, coalesced x)
+  if (single && stream && line_mode != 2 && launch_precond_slab(a, s)) return;
   if (single && stream) {
     // streaming fused path (3D): first direction y (PRO, coalesced), then x, then z (EPI)
     const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};

@@ -79,6 +79,9 @@ struct PrecArgs {
   int update;                     // apply x += alpha p, r -= alpha q first (if !pcg->first)
 };
 void launch_precond(const PrecArgs& a, cudaStream_t s);
+// 3D single patch: the three direction sweeps as shared-memory slabs (slab.cu); false if a
+// line set does not fit in shared memory (caller falls back to the streamed sweeps)
+bool launch_precond_slab(const PrecArgs& a, cudaStream_t s);
 
 struct VecArgs {
   GridDesc g;
