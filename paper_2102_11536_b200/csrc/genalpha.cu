@@ -936,11 +936,22 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       Lf.resize((size_t)(pp.bd[d] + sh.p + 1) * (sh.p + 1), 0.0);  // P zero rows for the backward sweep
       pp.hL[d] = Lf;
       pp.hdiag[d] = diag;
-      // chunks per line: enough threads (slots x chunks) to fill the GPU, <= 64
-      long long slots = (long long)sh.nvec * sh.k;
-      for (int e = 0; e < sh.dim; ++e)
-        if (e != d) slots *= pp.bd[e];
-      const int ctarget = (int)std::max(2LL, std::min(64LL, (150000 + slots - 1) / slots));
+      // chunks per line: enough threads (slots x chunks) to fill the GPU, <= 64; the
+      // slots of all patches run in one launch (additive Schwarz)
+      long long slots = 0;
+      for (const PrecPatch& q : ctx->prec) {
+        long long sl = (long long)sh.nvec * sh.k;
+        for (int e = 0; e < sh.dim; ++e)
+          if (e != d) sl *= q.bd[e];
+        slots += sl;
+      }
+      static long long thr_target = -1;
+      if (thr_target < 0) {
+        const char* e = getenv("GA_CHUNK_THREADS");
+        thr_target = e ? atoll(e) : 150000;
+      }
+      const long long tt = thr_target;  // measured on C5: more chunks (shorter serial chains) is faster
+      const int ctarget = (int)std::max(2LL, std::min(64LL, (tt + slots - 1) / slots));
       pp.sf[d] = make_sweep(Lf, pp.bd[d], sh.p, false, ctarget);
       pp.sb[d] = make_sweep(Lf, pp.bd[d], sh.p, true, ctarget);
       pp.Ff[d] = (double*)(ws + L.off_F[d][r]);

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 #include "spmv_core.cuh"
@@ -32,7 +33,7 @@ __global__ void __launch_bounds__(32 * G) k_spmv_sm(SpmvArgs a) {
   double dots[KK];
 #pragma unroll
   for (int j = 0; j < KK; ++j) dots[j] = 0.0;
-  spmv_block<P, NC, KK, ELASTIC, G>(a, blockIdx.x, smem_spmv, dots);
+  spmv_block<P, NC, KK, ELASTIC, G, false>(a, blockIdx.x, smem_spmv, dots);
   if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) {
     // per-block partial sums; the scalar step runs in k_spmv_fin (one block),
     // which avoids a fence + same-address atomic per block
@@ -109,6 +110,11 @@ static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
     const long long nrb = (a.g.npts + 31) / 32;
     if (a.elastic) {
       if constexpr (NC == 3) launch_sm<P, 3, KK, true, 4>(a, (unsigned int)((nrb + 3) / 4), s);
+    } else if (NC == 3) {
+      static int g3 = -1;  // warps per block of the 3-component (elastic) mass SpMV
+      if (g3 < 0) { const char* e = getenv("GA_SPMV_G3"); g3 = e ? atoi(e) : 8; }
+      if (g3 == 4) launch_sm<P, NC, KK, false, 4>(a, (unsigned int)((nrb + 3) / 4), s);
+      else launch_sm<P, NC, KK, false, 8>(a, (unsigned int)((nrb + 7) / 8), s);
     } else {
       launch_sm<P, NC, KK, false, 8>(a, (unsigned int)((nrb + 7) / 8), s);
     }

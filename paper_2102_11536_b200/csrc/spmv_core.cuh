@@ -27,7 +27,9 @@ __device__ __forceinline__ void load_row(const double* __restrict__ p, double (&
 // shared-memory slice (__syncwarp only) while the next line's window and
 // coefficients are prefetched into registers.  Warps are independent: no
 // block barrier, so many row blocks are in flight per SM.
-template <int P, int NC, int KK, bool ELASTIC, int G>
+// FUSE: the fused PCG direction update (a.fuse_p) is compiled in (persistent solver only);
+// the standalone kernel never uses it, which saves the p_old prefetch registers.
+template <int P, int NC, int KK, bool ELASTIC, int G, bool FUSE = true>
 __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, double* smem_spmv, double (&dots)[KK]) {
   constexpr int BR = 32;
   constexpr int W = 2 * P + 1, WN = BR + 2 * P;
@@ -49,7 +51,7 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   const double* xin = a.x;
   const double* __restrict__ cslice = a.coef + (icl >> 5) * NCF * S * 32 + (icl & 31);
   // fused PCG direction: the input window is p_new = z + beta p_old (z on the first iteration)
-  const bool fuse = a.mode == SPMV_PQ && a.fuse_p;
+  const bool fuse = FUSE && a.mode == SPMV_PQ && a.fuse_p;
   const bool mix = fuse && !a.fpfirst;
   if (fuse) xin = a.z;
   // raw window loads (the p_old part is combined when the window is staged,
