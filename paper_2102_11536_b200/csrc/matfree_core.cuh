@@ -92,7 +92,7 @@ __device__ __forceinline__ void mf_finish(const SpmvArgs& a, double (&dots)[KK])
 // 3D
 // ---------------------------------------------------------------------------
 template <int P, int KK, bool STIFF, int DX, int DY, int NT>
-__global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
+__global__ void __launch_bounds__(NT, (STIFF || P <= 4) ? 1 : 2) k_mf3(SpmvArgs a, int ZL, int nzc) {
   using L = Mf3Shape<P, KK, STIFF, DX, DY>;
   constexpr int P1 = L::P1, IX = L::IX, IY = L::IY, EY = L::EY, QX = L::QX, PLANE = L::PLANE;
   if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(NT) k_mf3(SpmvArgs a, int ZL, int nzc) {
       for (int i = tid; i < L::ACCS; i += NT) {
         const int j = i % KK, bxl = (i / KK) % DX, byl = i / (KK * DX);
         double r0 = 0.0, r1 = 0.0;
-#pragma unroll
+        constexpr int XB_UNROLL = P <= 4 ? P + 1 : 1;  // full unroll costs ~80 registers at high p
+#pragma unroll XB_UNROLL
         for (int e2 = 0; e2 <= P; ++e2) {
           const int exl = bxl + e2;
           const int u = P - e2;  // local index of basis bx within element exl (zero rows outside)
@@ -507,7 +508,8 @@ __global__ void __launch_bounds__(NT) k_mf2(SpmvArgs a, int YL, int nyc) {
       for (int i = tid; i < L::ACCS; i += NT) {
         const int j = i % KK, bxl = i / KK;
         double r0 = 0.0, r1 = 0.0;
-#pragma unroll
+        constexpr int XB_UNROLL = P <= 4 ? P + 1 : 1;  // full unroll costs ~80 registers at high p
+#pragma unroll XB_UNROLL
         for (int e2 = 0; e2 <= P; ++e2) {
           const int exl = bxl + e2, ex = exb + exl;
           if (ex < 0 || ex >= n) continue;

@@ -14,8 +14,11 @@ constexpr size_t MF_SMEM_SM = 228 * 1024;
 
 template <int P, int KK, bool STIFF>
 static unsigned int mf3_go(const SpmvArgs& a, cudaStream_t s, bool launch) {
-  constexpr int DX = 8, DY = 8, NT = 128;
+  constexpr int DX = 8, DY = 8;
   using L = Mf3Shape<P, KK, STIFF, DX, DY>;
+  // one thread per (x Gauss point, rhs) of the y walk (phase c), rounded to warps, >= 128
+  constexpr int NTW = ((L::QX * KK + 31) / 32) * 32;
+  constexpr int NT = NTW < 128 ? 128 : NTW;
   if constexpr (L::BYTES > MF_SMEM_MAX) {
     return 0;
   } else {
@@ -23,7 +26,7 @@ static unsigned int mf3_go(const SpmvArgs& a, cudaStream_t s, bool launch) {
     const int tx = (g.nx + DX - 1) / DX, ty = (g.ny + DY - 1) / DY;
     const long long tiles = (long long)tx * ty * a.nvec;
     // chunking from the 1-rhs footprint: every sub-batch must use the same blocks (partial sums)
-    const int occ = std::max(1, std::min(2048 / NT, (int)(MF_SMEM_SM / (Mf3Shape<P, 1, STIFF, DX, DY>::BYTES + 1024))));
+    const int occ = std::max(1, std::min(2048 / 128, (int)(MF_SMEM_SM / (Mf3Shape<P, 1, STIFF, DX, DY>::BYTES + 1024))));
     const long long target = 2LL * 148 * occ;
     int nzc = (int)std::min<long long>((target + tiles - 1) / tiles, std::max(1, g.nz / (2 * P)));
     nzc = std::max(1, nzc);
