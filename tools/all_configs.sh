@@ -1,8 +1,28 @@
 #!/bin/bash
-# One bench line per BASELINE config (writes profiles/<tag>_configs.jsonl)
+# One bench line per BASELINE config and sweep point (writes gpurun_out/<tag>_configs.jsonl)
 tag=${1:-r01}
 out=gpurun_out/${tag}_configs.jsonl
 : > $out
-for c in "--config c1 --k 2" "--config c1 --k 1" "--config c2" "--config c3 --p 2 --n 32" "--config c3 --p 2 --n 192" "--config c3 --p 3 --n 128" "--config c3 --p 4 --n 96" "--config c3 --p 2 --n 96 --k 3 --rho 1.0" "--config c3 --p 6 --n 48" "--config c4" "--config c5"; do
-  timeout 900 python bench.py $c --steps 10 --warmup 3 --no-cpu-baseline --kernel-reps 3 >> $out 2> gpurun_out/err.txt || echo "{\"failed\": \"$c\"}" >> $out
-done
+run() {
+  timeout 1200 python bench.py "$@" --no-cpu-baseline --kernel-reps 3 >> $out 2> gpurun_out/err_${tag}.txt || echo "{\"failed\": \"$*\"}" >> $out
+}
+run --config c1 --k 2 --steps 10 --warmup 3
+run --config c1 --k 1 --steps 10 --warmup 3
+run --config c2 --steps 10 --warmup 3
+run --config c3 --p 2 --n 32 --steps 10 --warmup 3
+run --config c3 --p 2 --n 192 --steps 10 --warmup 3
+run --config c3 --p 3 --n 128 --steps 10 --warmup 3
+run --config c3 --p 3 --n 192 --steps 5 --warmup 3 --lam-iters 20
+run --config c3 --p 4 --n 96 --steps 10 --warmup 3
+run --config c3 --p 4 --n 96 --steps 5 --warmup 3 --op-mode 2
+run --config c3 --p 4 --n 192 --steps 5 --warmup 3 --lam-iters 20
+run --config c3 --p 5 --n 128 --steps 5 --warmup 3 --lam-iters 20
+run --config c3 --p 5 --n 192 --steps 3 --warmup 3 --lam-iters 8
+run --config c3 --p 6 --n 48 --steps 10 --warmup 3
+run --config c3 --p 6 --n 96 --steps 5 --warmup 3 --lam-iters 20
+run --config c3 --p 6 --n 96 --steps 3 --warmup 3 --lam-iters 8 --op-mode 2
+run --config c3 --p 6 --n 192 --steps 3 --warmup 3 --lam-iters 8
+run --config c3 --p 2 --n 96 --k 3 --rho 1.0 --steps 10 --warmup 3
+run --config c3 --p 2 --n 96 --k 1 --rho 0.5 --steps 10 --warmup 3
+run --config c4 --steps 10 --warmup 3
+run --config c5 --steps 10 --warmup 3
