@@ -94,7 +94,10 @@ typedef struct {
                         /* 1: assembled column-index-free stencils (2p+1)^dim per row;  */
                         /* 2: matrix-free sum factorisation from the Gauss-point data   */
                         /*    (single patch only; the elastic K stays a stencil);       */
-                        /* 0: auto = the measured-faster of the two      */
+                        /* 3: half-symmetric stencils, offsets o >= 0 only (same bytes  */
+                        /*    per apply, half the memory; the elastic K stays full);    */
+                        /* 0: auto = full stencils if they fit in ~150 GB, else half-   */
+                        /*    symmetric, else matrix-free (measured, R14)     */
 } ga_desc;
 
 typedef struct {
@@ -192,6 +195,8 @@ ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
 int ga_uses_persistent_solver(const ga_ctx* ctx);
 /* 1 if the context applies M (and the scalar K) matrix-free (op_mode 2, or op_mode 0's pick). */
 int ga_uses_matrix_free(const ga_ctx* ctx);
+/* Operator representation in use: 1 full stencils, 2 matrix-free, 3 half-symmetric stencils. */
+int ga_operator_mode(const ga_ctx* ctx);
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream);
 
 void ga_destroy(ga_ctx* ctx);

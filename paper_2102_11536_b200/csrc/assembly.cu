@@ -217,6 +217,13 @@ __global__ void k_contract_final(const double* __restrict__ in, const double* __
   for (int q = qs; q < qe; ++q) s = fma(__ldg(Ai + (q - qs)), __ldg(src + (long long)(q - f.qoff) * sq), s);
   // stencil offset index, lexicographic with x fastest
   long long olin = (oo[0] + f.p) + (long long)W1 * ((oo[1] + f.p) + (DIM == 3 ? (long long)W1 * (oo[2] + f.p) : 0));
+  if (f.half) {  // o >= 0 only (index o - S/2), rows shifted by the zero guard
+    const long long Sh = (f.S + 1) / 2, hl = olin - f.S / 2;
+    if (hl < 0) return;
+    const long long rr = grow + f.hguard;
+    coef[((rr >> 5) * Sh + hl) * 32 + (rr & 31)] += s;
+    return;
+  }
   // blocked layout: 32-row slices, all NCF*S offsets of a slice contiguous
   coef[((grow >> 5) * f.ncf * f.S + (long long)f.ab * f.S + olin) * 32 + (grow & 31)] += s;
 }

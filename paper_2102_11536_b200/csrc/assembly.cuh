@@ -34,6 +34,8 @@ struct FinalDesc {
   long long S;                 // offsets per coefficient array
   int ncf, ab;                 // coefficient arrays per row slice (1 or 9) and the target block
   const unsigned char* mask;
+  int half;                    // half-symmetric layout: offsets o >= 0 only, rows shifted by hguard
+  long long hguard;
 };
 
 void launch_geometry(const AsmPatch& P, int dim, int qa, int nqs, double* geo, long long gstride, double* minmax,

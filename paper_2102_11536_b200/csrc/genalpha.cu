@@ -77,6 +77,7 @@ struct ga_ctx {
   bool nograph = false;  // GA_NO_GRAPH=1: direct launches, host-driven PCG loop (profiling/debug)
   bool persist = false;  // small single-patch scalar problems: one cooperative kernel per solve
   bool mf = false;       // matrix-free M (and scalar K): sum factorisation from Gauss-point data
+  bool half = false;     // half-symmetric stencils (offsets o >= 0, zero guard of g.guard rows)
   double *mfWM = nullptr, *mfWK = nullptr, *mftv = nullptr, *mftd = nullptr, *diagM = nullptr;
   long long mfws = 0;    // Gauss points (n(p+1))^dim
   long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
@@ -119,9 +120,10 @@ struct Shape {
   std::vector<long long> local;
   int pmin[3], pmax[3];
   bool mf = false;     // matrix-free operators (op_mode 2, or auto)
+  bool half = false;   // half-symmetric stencils (op_mode 3, or auto)
 };
 
-bool mf_auto(const ga_desc* d);
+int op_auto(const ga_desc* d);
 
 ga_status validate(const ga_desc* d, ga_ctx* ctx) {
   if (!d) { seterr(ctx, "desc is NULL"); return GA_ERR_ARG; }
@@ -136,7 +138,7 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
   if (!(d->pcg_refine_rtol >= 0.0) || d->pcg_refine_rtol >= 1.0) { seterr(ctx, "pcg_refine_rtol must be in [0,1)"); return GA_ERR_ARG; }
   if (!(d->pcg_rtol > 0.0) || d->pcg_maxit < 1) { seterr(ctx, "pcg_rtol > 0 and pcg_maxit >= 1 required"); return GA_ERR_ARG; }
   if (d->param_set != 0 && d->param_set != 1) { seterr(ctx, "param_set must be 0 or 1"); return GA_ERR_ARG; }
-  if (d->op_mode < 0 || d->op_mode > 2) { seterr(ctx, "op_mode must be 0, 1 or 2"); return GA_ERR_ARG; }
+  if (d->op_mode < 0 || d->op_mode > 3) { seterr(ctx, "op_mode must be 0, 1, 2 or 3"); return GA_ERR_ARG; }
   if (d->op_mode == 2 && d->npatch != 1) { seterr(ctx, "op_mode 2 (matrix-free) supports a single patch"); return GA_ERR_ARG; }
   double a[KMAX], b[KMAX], g[KMAX], f[KMAX], th;
   int rc = scheme_params(d->k, d->rho_b, d->rho_s, d->param_set, a, b, g, f, &th);
@@ -157,7 +159,11 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
 // Global masked grid, boxes, maps.
 ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_conformity) {
   sh.dim = d->dim; sh.nvec = d->ncomp; sh.p = d->p; sh.n = d->n; sh.m = d->n + d->p; sh.k = d->k; sh.W1 = 2 * d->p + 1;
-  sh.mf = d->op_mode == 2 || (d->op_mode == 0 && mf_auto(d));
+  {
+    const int pick = d->op_mode == 0 ? op_auto(d) : d->op_mode;
+    sh.mf = pick == 2;
+    sh.half = pick == 3;
+  }
   sh.S = (long long)sh.W1 * sh.W1 * (sh.dim == 3 ? sh.W1 : 1);
   const int m = sh.m, dim = sh.dim;
   int cmax[3] = {0, 0, 0};
@@ -272,15 +278,19 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
 
 // op_mode 0: which representation is faster, from the measured operator times
 // (DESIGN.md §6 "Stencil vs matrix-free"); multi-patch grids always use stencils.
-// Measured (profiles/r01_matfree.md): the stencil SpMV at 0.8-0.97 of HBM bandwidth beats
-// the fp64-bound sum factorisation at every degree where the stencils fit, so op_mode 0
-// takes matrix-free only when the assembled M and K would not fit in the B200's HBM.
-bool mf_auto(const ga_desc* d) {
-  if (d->npatch != 1) return false;
+// op_mode 0 (R14, §6 "Stencil vs matrix-free"): measured, the stencil SpMV at
+// 0.8-0.97 of HBM bandwidth beats the fp64-bound sum factorisation at every degree where the
+// stencils fit, so: full stencils if M and K fit in ~150 GB, else half-symmetric stencils
+// (same bytes streamed per apply, half the footprint), else matrix-free.
+int op_auto(const ga_desc* d) {
   const double W1 = 2.0 * d->p + 1.0, S = d->dim == 3 ? W1 * W1 * W1 : W1 * W1;
-  const double npts = std::pow((double)(d->n + d->p - 2), d->dim);
-  const double stencil_bytes = 8.0 * S * npts * (d->ncomp == 3 ? 10.0 : 2.0);
-  return stencil_bytes > 150e9;
+  const double npts = std::pow((double)((d->n + d->p - 1) * 2), d->dim);  // generous (multi-patch box)
+  const double nsp = d->npatch == 1 ? std::pow((double)(d->n + d->p - 2), d->dim) : npts;
+  const double full = 8.0 * S * nsp * (d->ncomp == 3 ? 10.0 : 2.0);
+  const double half = 8.0 * nsp * (d->ncomp == 3 ? (S + 1) / 2 + 9 * S : S + 1);
+  if (full <= 150e9) return 1;
+  if (half <= 150e9) return 3;
+  return d->npatch == 1 ? 2 : 3;
 }
 
 size_t sweep_bytes(int n, int p) {
@@ -293,9 +303,11 @@ Layout make_layout(const Shape& sh) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
   const long long npts = sh.g.npts;
-  const bool mfK = sh.mf && sh.nvec == 1;  // the elastic K stays a stencil
-  L.off_coefM = take(sh.mf ? 0 : sizeof(double) * sh.S * sh.g.cs);
-  L.off_coefK = take(mfK ? 0 : sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1));
+  const bool mfK = sh.mf && sh.nvec == 1;  // the elastic K stays a full stencil
+  const long long Sh = (sh.S + 1) / 2, hrows = (npts + sh.g.guard + 31) / 32 * 32;
+  const size_t mbytes = sh.half ? sizeof(double) * Sh * hrows : sizeof(double) * sh.S * sh.g.cs;
+  L.off_coefM = take(sh.mf ? 0 : mbytes);
+  L.off_coefK = take(mfK ? 0 : (sh.nvec == 3 ? sizeof(double) * sh.S * sh.g.cs * 9 : mbytes));
   {
     const long long nq = (long long)sh.n * (sh.p + 1);
     const long long nqd = sh.dim == 3 ? nq * nq * nq : nq * nq;
@@ -355,7 +367,7 @@ size_t asm_fixed_bytes(const Shape& sh) {
 
 __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, int loz, const double* d0,
                           const double* d1, const double* d2, const double* coefM, const double* diagM, long long S,
-                          int nx, int ny, const unsigned char* mask) {
+                          int nx, int ny, const unsigned char* mask, long long hguard) {
   const long long nbox = (long long)bx * by * bz;
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nbox) return;
@@ -365,7 +377,10 @@ __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, i
   if (!mask || mask[gi]) {
     const double dh = d0[ix] * d1[iy] * (d2 ? d2[iz] : 1.0);
     // diag(M): matrix-free array, or the centre offset of the blocked stencil layout
-    const double D = diagM ? diagM[gi] : coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)];
+    const long long hr = gi + hguard;  // half-symmetric layout: centre offset = index 0
+    const double D = diagM ? diagM[gi]
+                           : (hguard >= 0 ? coefM[((hr >> 5) * ((S + 1) / 2)) * 32 + (hr & 31)]
+                                          : coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)]);
     v = sqrt(dh / D);  // s = sqrt(Dh / D): calM^{-1} = S Mh^{-1} S
   }
   s[e] = v;
@@ -417,6 +432,7 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
   a.x = x; a.y = y; a.b = c->b;
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
+  if (c->half && !a.elastic) { a.half = 1; a.hguard = c->g.guard; }
   if (c->mf && !a.elastic) {
     a.mf = 1; a.mfstiff = which; a.mfn = c->n; a.mfj0 = 0;
     a.mfW = which == 0 ? c->mfWM : c->mfWK; a.mfws = c->mfws;
@@ -600,8 +616,10 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   if (off > scratch_bytes) { seterr(ctx, "scratch too small (slab)"); return GA_ERR_OOM; }
 
   const bool mfK = sh.mf && sh.nvec == 1;
-  if (!sh.mf) CK(cudaMemsetAsync(ctx->coefM, 0, sizeof(double) * sh.S * sh.g.cs, s));
-  if (!mfK) CK(cudaMemsetAsync(ctx->coefK, 0, sizeof(double) * sh.S * sh.g.cs * (sh.nvec == 3 ? 9 : 1), s));
+  const long long Sh = (sh.S + 1) / 2, hrows = (sh.g.npts + sh.g.guard + 31) / 32 * 32;
+  const size_t mbytes = sh.half ? sizeof(double) * Sh * hrows : sizeof(double) * sh.S * sh.g.cs;
+  if (!sh.mf) CK(cudaMemsetAsync(ctx->coefM, 0, mbytes, s));
+  if (!mfK) CK(cudaMemsetAsync(ctx->coefK, 0, sh.nvec == 3 ? sizeof(double) * sh.S * sh.g.cs * 9 : mbytes, s));
   // term list: (target block pointer, spec, derivative flags per direction)
   struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; int ab; };
   std::vector<Term> terms;
@@ -690,6 +708,8 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         f.ncf = (t.coef == ctx->coefK && sh.nvec == 3) ? 9 : 1;
         f.ab = t.ab;
         f.mask = ctx->mask;
+        f.half = (sh.half && f.ncf == 1) ? 1 : 0;  // the elastic K stays full
+        f.hguard = sh.g.guard;
         if (dim == 3) {
           ContractDesc c2;
           memset(&c2, 0, sizeof(c2));
@@ -864,6 +884,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->coefM = (double*)(ws + L.off_coefM);
   ctx->coefK = (double*)(ws + L.off_coefK);
   ctx->mf = sh.mf;
+  ctx->half = sh.half;
   if (sh.mf) {
     const long long nq = (long long)sh.n * (sh.p + 1);
     ctx->mfws = sh.dim == 3 ? nq * nq * nq : nq * nq;
@@ -973,7 +994,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     const double* center = ctx->coefM;  // blocked layout: k_scaling indexes offset S/2
     k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
                                                                  pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
-                                                                 center, ctx->diagM, ctx->S, sh.g.nx, sh.g.ny, ctx->mask);
+                                                                 center, ctx->diagM, ctx->S, sh.g.nx, sh.g.ny, ctx->mask,
+                                                                 sh.half ? sh.g.guard : -1);
     CKD(cudaGetLastError());
     CKD(cudaStreamSynchronize(s));  // tmp reused by the next patch
   }
@@ -987,7 +1009,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     // latency-bound regime: little data per PCG phase (C2-like); bandwidth-bound grids keep the graph path
     const bool small = (long long)sh.g.npts * sh.k <= 600000 && (double)sh.S * sh.g.npts * 8.0 <= 64e6;
     const bool want = pe ? (*pe != '0') : small;
-    ctx->persist = want && !ctx->mf && persist_supported(persist_args(ctx));
+    ctx->persist = want && !ctx->mf && !ctx->half && persist_supported(persist_args(ctx));
     const char* te = getenv("GA_TRACE");
     if (te && *te && *te != '0') {
       cudaMalloc(&ctx->trace, 8192 * sizeof(long long));  // debug only
@@ -1250,6 +1272,7 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
 
 int ga_uses_persistent_solver(const ga_ctx* ctx) { return ctx && ctx->persist ? 1 : 0; }
 int ga_uses_matrix_free(const ga_ctx* ctx) { return ctx && ctx->mf ? 1 : 0; }
+int ga_operator_mode(const ga_ctx* ctx) { return !ctx ? 0 : (ctx->mf ? 2 : (ctx->half ? 3 : 1)); }
 
 // debug: copy the persistent-solver trace (GA_TRACE=1) to the host; returns slots copied
 int ga_debug_trace(ga_ctx* ctx, long long* host, int n) {

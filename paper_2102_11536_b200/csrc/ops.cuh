@@ -42,6 +42,10 @@ struct SpmvArgs {
   long long mfws;      // nq^d, nq = n (p+1) (global tensor Gauss grid, x fastest)
   const double* mfv;   // 1D basis values  [nq][p+1]  (local function a of element q/(p+1))
   const double* mfd;   // 1D derivatives   [nq][p+1]
+  // half-symmetric stencil (half = 1): offsets o >= 0 only, rows shifted by a zero guard of
+  // hguard rows (spmv_core.cuh spmv_block_half); not for the elastic (3x3-block) K
+  int half;
+  long long hguard;
 };
 void launch_spmv(const SpmvArgs& a, cudaStream_t s);
 // matrix-free variants (matfree.cu): the same contract as launch_spmv for a.mf = 1

@@ -45,6 +45,24 @@ __global__ void __launch_bounds__(32 * G) k_spmv_sm(SpmvArgs a) {
   }
 }
 
+template <int P, int NC, int KK, int G>
+__global__ void __launch_bounds__(32 * G) k_spmv_half(SpmvArgs a) {
+  if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
+  count_launch(a.st);
+  extern __shared__ double smem_spmv[];
+  double dots[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) dots[j] = 0.0;
+  spmv_block_half<P, NC, KK, G>(a, blockIdx.x, smem_spmv, dots);
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) {
+    block_sum<KK>(dots);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < KK; ++j) a.partial[(size_t)blockIdx.x * KK + j] = dots[j];
+    }
+  }
+}
+
 // Fixed-order sum of the SpMV block partials and the PCG scalar step:
 // SPMV_PQ: alpha_j = r.z / p.q (F2); SPMV_TRUERES: restart of the refinement phase.
 template <int KK>
@@ -105,7 +123,26 @@ static void launch_sm(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
 }
 
 template <int P, int NC, int KK>
+static void launch_half(const SpmvArgs& a, cudaStream_t s) {
+  constexpr int G = 8, BR = 32, WN = BR + 2 * P;
+  constexpr size_t bytes = sizeof(double) * (2 * 2 * G * NC * WN * KK);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmv_half<P, NC, KK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    attr = true;
+  }
+  const long long nrb = (a.g.npts + 31) / 32;
+  const unsigned int nb = (unsigned int)((nrb + G - 1) / G);
+  k_spmv_half<P, NC, KK, G><<<nb, 32 * G, bytes, s>>>(a);
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) k_spmv_fin<KK><<<1, 1024, 0, s>>>(a, nb);
+}
+
+template <int P, int NC, int KK>
 static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
+  if (a.half && !a.elastic) {
+    launch_half<P, NC, KK>(a, s);
+    return;
+  }
   {
     const long long nrb = (a.g.npts + 31) / 32;
     if (a.elastic) {

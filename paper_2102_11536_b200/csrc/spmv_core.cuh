@@ -169,5 +169,124 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
 }
 
 
+// Half-symmetric stencil (SURVEY §8a a1 option): only the
+// offsets o >= 0 (lexicographic) are stored, coef_h[(row + G)/32][o - S/2][(row + G)%32] with a
+// zero guard of G rows before row 0; the other half follows from symmetry,
+//   c(i, -o) = c(i - s(o), o),  s(o) = o1 + o2 sy + o3 sz  (M, K symmetric).
+// The warp walks the (W3 W + 1)/2 offset lines (o3, o2) >= (0, 0); per line it stages the input
+// window at +line (own terms, coefficients of its own rows) and at -line (mirror terms,
+// coefficients of the rows i - s(o): one shifted, still contiguous 32-row slice per o1).
+template <int P, int NC, int KK, int G>
+__device__ __forceinline__ void spmv_block_half(const SpmvArgs& a, long long rbg, double* smem_spmv,
+                                                double (&dots)[KK]) {
+  constexpr int BR = 32;
+  constexpr int W = 2 * P + 1, WN = BR + 2 * P;
+  auto win = reinterpret_cast<double (*)[2][2][NC][WN][KK]>(smem_spmv);  // [G][buf][own/mirror][NC][WN][KK]
+  const GridDesc g = a.g;
+  const int r = threadIdx.x & 31, gq = threadIdx.x >> 5;
+  const long long rb = rbg * G + gq;
+  const long long i0 = rb * BR;
+  if (i0 >= g.npts) return;
+  const long long i = i0 + r;
+  const bool valid = i < g.npts;
+  const long long icl = valid ? i : (g.npts - 1);
+  const int W3 = (g.dim == 3) ? W : 1;
+  const int P3 = (g.dim == 3) ? P : 0;
+  const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+  const long long Sh = ((long long)W * W * W3 + 1) / 2;
+  const long long hg = a.hguard;
+  const int nlh = (W3 * W + 1) / 2;
+  const int c2 = P + W * P3;  // lin2 of the centre line
+  auto rowc = [&](long long row, long long hidx) -> double {  // coef_h of a (guard-shifted) row
+    const long long rr = row + hg;
+    return __ldg(a.coef + ((rr >> 5) * Sh + hidx) * 32 + (rr & 31));
+  };
+  auto fetch_win = [&](int t, int sign, int q, int c, double (&v)[KK]) {
+    const int lin2 = c2 + t, o3 = lin2 / W - P3, o2 = lin2 % W - P;
+    const long long pos = g.guard + i0 - P + q + sign * (o3 * sz + o2 * sy);
+    load_row<KK>(a.x + ((long long)c * g.padded + pos) * KK, v);
+  };
+  auto fetch_coef = [&](int t, double (&co)[W], double (&cm)[W]) {
+    const int lin2 = c2 + t, o3 = lin2 / W - P3, o2 = lin2 % W - P;
+    const long long sline = o3 * sz + o2 * sy;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const int o1 = u - P;
+      const long long hidx = o1 + (long long)W * t;
+      co[u] = (t > 0 || o1 >= 0) ? rowc(icl, hidx) : 0.0;
+      cm[u] = (t > 0 || o1 > 0) ? rowc(icl - (o1 + sline), hidx) : 0.0;
+    }
+  };
+  const bool two = r < 2 * P;
+  double acc[NC][KK];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
+  double pw[2][2][NC][KK];  // [own/mirror][first/second part of the window]
+  double cf[W], cm[W];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      fetch_win(0, sgn ? -1 : 1, r, c, pw[sgn][0][c]);
+      if (two) fetch_win(0, sgn ? -1 : 1, BR + r, c, pw[sgn][1][c]);
+    }
+  fetch_coef(0, cf, cm);
+  int buf = 0;
+  for (int t = 0; t < nlh; ++t) {
+#pragma unroll
+    for (int sgn = 0; sgn < 2; ++sgn)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          win[gq][buf][sgn][c][r][j] = pw[sgn][0][c][j];
+          if (two) win[gq][buf][sgn][c][BR + r][j] = pw[sgn][1][c][j];
+        }
+    double co[W], cmc[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) { co[u] = cf[u]; cmc[u] = cm[u]; }
+    __syncwarp();
+    if (t + 1 < nlh) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int sgn = 0; sgn < 2; ++sgn) {
+          fetch_win(t + 1, sgn ? -1 : 1, r, c, pw[sgn][0][c]);
+          if (two) fetch_win(t + 1, sgn ? -1 : 1, BR + r, c, pw[sgn][1][c]);
+        }
+      fetch_coef(t + 1, cf, cm);
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          acc[c][j] = fma(co[u], win[gq][buf][0][c][r + u][j], acc[c][j]);           // x[i + o]
+          acc[c][j] = fma(cmc[u], win[gq][buf][1][c][r + 2 * P - u][j], acc[c][j]);  // x[i - o]
+        }
+    }
+    buf ^= 1;
+  }
+  if (!valid) return;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+    double pv[KK];
+    if (a.mode == SPMV_PQ) load_row<KK>(a.x + base, pv);
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      double v = acc[c][j];
+      if (a.mode == SPMV_NEGB) v = -v;
+      else if (a.mode == SPMV_TRUERES) { v = a.b[base + j] - v; dots[j] = fma(v, v, dots[j]); }
+      else if (a.mode == SPMV_PQ) dots[j] = fma(pv[j], v, dots[j]);
+      a.y[base + j] = v;
+    }
+  }
+}
+
+
 
 }  // namespace ga

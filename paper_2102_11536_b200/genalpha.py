@@ -24,7 +24,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
 
 EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
-            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_destroy",
+            "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_operator_mode", "ga_destroy",
             "ga_last_error"]
 
 
@@ -77,6 +77,7 @@ def _load():
         "ga_profile_op": (c_int, [c_void_p, c_int, c_int, c_void_p]),
         "ga_uses_persistent_solver": (c_int, [c_void_p]),
         "ga_uses_matrix_free": (c_int, [c_void_p]),
+        "ga_operator_mode": (c_int, [c_void_p]),
         "ga_destroy": (None, [c_void_p]),
         "ga_last_error": (ctypes.c_char_p, [c_void_p]),
     }
@@ -229,6 +230,10 @@ class Context:
 
     def matrix_free(self):
         return bool(lib.ga_uses_matrix_free(self.ctx))
+
+    def operator_mode(self):
+        """1 full stencils, 2 matrix-free, 3 half-symmetric stencils."""
+        return int(lib.ga_operator_mode(self.ctx))
 
     def free_dof_map(self):
         ncomp = self.desc.ncomp

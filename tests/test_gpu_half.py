@@ -1,0 +1,84 @@
+"""GPU parity of the half-symmetric stencil layout (op_mode 3, SURVEY §8a a1 option
+coef(i,-o) = coef(i-o,+o)): operators element by element against the oracle and against
+the full-stencil path of the library, the preconditioner (diag(M) from the half layout),
+and trajectories in the relative M-norm.  Cases: 2D/3D, p = 1..6, ragged row blocks,
+k = 1..3, the elastic layout (mass half-symmetric, 3x3-block K full) and the masked
+multi-patch grid."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import precond
+
+from _helpers import Case, mnorm_rel, oracle_with_floor
+
+pytestmark = pytest.mark.gpu
+
+HALF_CASES = {
+    "2d_p1_n9": synth.config("c2", p=1, n=9),
+    "2d_p3_n10": synth.config("c2", n=10),
+    "3d_p2_n5": synth.config("c3", p=2, n=5),
+    "3d_p3_n4_k3": synth.config("c3", p=3, n=4, k=3),
+    "3d_p4_n3": synth.config("c3", p=4, n=3),
+    "3d_p6_n2": synth.config("c3", p=6, n=2),
+    "elastic_p2_n3": synth.config("c4", p=2, n=3),
+    "lshape_p2_n4": synth.config("c5", p=2, n=4),
+}
+
+
+@pytest.fixture(scope="module", params=sorted(HALF_CASES))
+def hcase(request):
+    c = Case(HALF_CASES[request.param], op_mode=3)
+    assert c.ctx.operator_mode() == 3
+    return c
+
+
+def test_half_operators_elementwise(hcase):
+    d = hcase.disc
+    rng = np.random.default_rng(27)
+    for which, A in (("M", d.M), ("K", d.K)):
+        x = rng.standard_normal(A.shape[0])
+        y = hcase.from_lib(hcase.ctx.apply(which, hcase.to_lib(x)))
+        ref = A @ x
+        scale = (abs(A) @ np.abs(x)).max()
+        assert np.abs(y - ref).max() <= 1e-13 * scale, which
+
+
+def test_half_preconditioner(hcase):
+    P = precond.SchwarzPreconditioner(hcase.disc)
+    x = np.random.default_rng(28).standard_normal(hcase.disc.M.shape[0])
+    y = hcase.from_lib(hcase.ctx.apply("Pinv", hcase.to_lib(x)))
+    ref = P(x)
+    assert np.abs(y - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["2d_p3_n10", "3d_p3_n4_k3", "lshape_p2_n4"])
+def test_half_equals_full(name):
+    a = Case(HALF_CASES[name], op_mode=1)
+    b = Case(HALF_CASES[name], op_mode=3)
+    x = np.random.default_rng(29).standard_normal(a.disc.M.shape[0])
+    for which in ("M", "K"):
+        ya = a.from_lib(a.ctx.apply(which, a.to_lib(x)))
+        yb = b.from_lib(b.ctx.apply(which, b.to_lib(x)))
+        assert np.abs(ya - yb).max() <= 1e-13 * np.abs(ya).max(), which
+
+
+@pytest.mark.parametrize("cfg,nsteps", [
+    (synth.config("c2", n=20), 40),
+    (synth.config("c3", p=3, n=5, k=2, rho=0.5), 20),
+    (synth.config("c3", p=5, n=3, k=1, rho=1.0), 20),
+    (synth.config("c4", p=2, n=3), 10),
+    (synth.config("c5", p=3, n=6), 20),
+])
+def test_half_trajectory(cfg, nsteps):
+    c = Case(cfg, op_mode=3)
+    d = c.disc
+    u0 = c.u0()
+    c.ctx.set_state(c.to_lib(u0))
+    c.ctx.advance(nsteps)
+    st = c.ctx.stats()
+    assert st.status == 0 and st.steps == nsteps
+    u, v, a = (c.from_lib(t) for t in c.ctx.get_state())
+    ref, floor = oracle_with_floor(d, cfg["k"], cfg["rho"], c.dt, u0, np.zeros_like(u0), nsteps, case=c)
+    errs = [mnorm_rel(d.M, x, y) for x, y in zip((u, v, a), ref[:3])]
+    assert all(e < max(1e-10, 10 * f) for e, f in zip(errs, floor)), (errs, floor)
