@@ -306,6 +306,12 @@ def run_ours(args, rank, world, local_rank):
              3: "k_stage(predictor pass)", 5: "k_p_update"}
     persistent = ctx.persistent()
     mfree = ctx.matrix_free()
+    opmode = ctx.operator_mode()  # 1 full stencils, 2 matrix-free, 3 half-symmetric stencils
+    if opmode == 3:  # compulsory coefficient bytes of the half layout: (S + 1) / 2 per row
+        info["S"] = (info["S"] + 1) // 2
+        names[0] = "k_spmv_half(M)+p.q"
+        if nc == 1:
+            names[1] = "k_spmv_half(K)"
     if mfree:
         names[0] = "k_mf3/k_mf2(M, matrix-free)+p.q"
         if nc == 1:
@@ -315,6 +321,8 @@ def run_ours(args, rank, world, local_rank):
     L = loop_iters / steps  # lock-stepped PCG iterations per step (one solve set per step)
     nsolve_phases = 2 if True else 1  # main phase + refinement restart
     info_bytes = {op: algorithmic_bytes(op, info) for op in (0, 1, 2, 3)}
+    if opmode == 3 and nc == 3:  # the elastic K stays a full 3x3-block stencil
+        info_bytes[1] = algorithmic_bytes(1, dict(info, S=(2 * cfg["p"] + 1) ** cfg["dim"]))
     info_bytes[5] = 24 * info["nvec"] * info["k"] * info["npts"]
     # whole solve: L SpMV + 1 true-residual SpMV, L + 2 preconditioner applications, L direction updates
     info_bytes[6] = (L + 1) * info_bytes[0] + (L + 2) * info_bytes[2] + L * info_bytes[5]
@@ -413,7 +421,7 @@ def run_ours(args, rank, world, local_rank):
                            "l2": "flushed between timed steps (256 MiB write), working set "
                                  f"{ctx.workspace.numel() / 2**20:.0f} MiB",
                            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                           "operators": "matrix-free" if mfree else "stencil"},
+                           "operators": {1: "stencil", 2: "matrix-free", 3: "half-symmetric stencil"}[opmode]},
                 "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")}}
         if world == 1 and not args.no_cpu_baseline:
