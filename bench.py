@@ -259,7 +259,11 @@ def run_ours(args, rank, world, local_rank):
     u0_np = np.concatenate([np.array([prob["u0"][int(v // mpow)][int(v % mpow), c] for v in fmap])
                             for c in range(nc)])
     u0 = torch.tensor(u0_np, dtype=torch.float64, device=dev)
-    ctx.set_state(u0)
+    v0 = None
+    if prob.get("v0") is not None:  # E1: V0 != 0 (initial chain with a velocity, R3)
+        v0 = torch.tensor(np.concatenate([np.array([prob["v0"][int(v // mpow)][int(v % mpow), c] for v in fmap])
+                                          for c in range(nc)]), dtype=torch.float64, device=dev)
+    ctx.set_state(u0, v0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         ctx.advance(1)

@@ -24,7 +24,7 @@ import numpy as np
 
 __all__ = [
     "greville_1d", "control_net", "lshape_patches", "sine_modes", "eval_modes",
-    "sinpi_product", "CONFIGS", "config", "make_problem",
+    "sinpi_product", "e1_exact", "CONFIGS", "config", "make_problem",
 ]
 
 
@@ -116,7 +116,19 @@ CONFIGS = {
                lam=1.0, mu=1.0, density=1.0),
     "c5": dict(name="c5", dim=2, ncomp=1, p=3, n=512, noise=0.1, seed=5, init="modes",
                init_seed=105, k=2, rho=0.3, steps=200, cfl_frac=0.5, lshape=True),
+    # the paper's own order-4 experiment (§6.1), unit square,
+    # p=7, C^6, 100x100 elements, T = 0.1, u = sin(10 pi x) sin(10 pi y)[cos + sin](10 sqrt2 pi t)
+    # (P:831 read as sin(10 pi y)); u0 = sin sin, v0 = 10 sqrt2 pi sin sin
+    "e1": dict(name="e1", dim=2, ncomp=1, p=7, n=100, noise=0.0, seed=1, init="e1",
+               init_seed=0, k=2, rho=0.0, steps=100, cfl_frac=0.5, lshape=False, T=0.1),
 }
+
+
+def e1_exact(pts: np.ndarray, t: float):
+    """(u, u_t) of the E1 closed form (reading G24) at points pts (N, 2), time t."""
+    w = 10.0 * np.sqrt(2.0) * np.pi
+    sp = np.sin(10.0 * np.pi * pts[:, 0]) * np.sin(10.0 * np.pi * pts[:, 1])
+    return sp * (np.cos(w * t) + np.sin(w * t)), sp * w * (np.cos(w * t) - np.sin(w * t))
 
 
 def config(name: str, **over) -> dict:
@@ -137,11 +149,18 @@ def make_problem(cfg: dict):
         patches = [((0,) * dim, control_net(dim, p, n, cfg["noise"], cfg["seed"]))]
     ncomp = cfg.get("ncomp", 1)
     u0 = []
+    v0 = None
     if cfg["init"] == "sinpi":
         for _, ctrl in patches:
             u0.append(np.stack([sinpi_product(ctrl)] * ncomp, axis=1))
+    elif cfg["init"] == "e1":
+        v0 = []
+        for _, ctrl in patches:
+            uu, vv = e1_exact(ctrl, 0.0)
+            u0.append(uu[:, None])
+            v0.append(vv[:, None])
     else:
         amps = [sine_modes(cfg["init_seed"] + 1000 * c) for c in range(ncomp)]
         for _, ctrl in patches:
             u0.append(np.stack([eval_modes(a, ctrl) for a in amps], axis=1))
-    return dict(patches=patches, u0=u0)
+    return dict(patches=patches, u0=u0, v0=v0)
