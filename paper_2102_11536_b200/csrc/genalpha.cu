@@ -79,6 +79,7 @@ struct ga_ctx {
   bool mf = false;       // matrix-free M (and scalar K): sum factorisation from Gauss-point data
   bool half = false;     // half-symmetric stencils (offsets o >= 0, zero guard of g.guard rows)
   double *mfWM = nullptr, *mfWK = nullptr, *mftv = nullptr, *mftd = nullptr, *diagM = nullptr;
+  double *mpT1 = nullptr, *mpT2 = nullptr, *mpT3 = nullptr;  // 3D multi-pass mass intermediates
   long long mfws = 0;    // Gauss points (n(p+1))^dim
   long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
 };
@@ -103,7 +104,7 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t off_coefM, off_coefK, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
-      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag;
+      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
 };
@@ -315,6 +316,12 @@ Layout make_layout(const Shape& sh) {
     L.off_mfWK = take(mfK ? sizeof(double) * nqd * (sh.dim == 3 ? 6 : 3) : 0);
     L.off_mftab = take(sh.mf ? sizeof(double) * 2 * nq * (sh.p + 1) : 0);
     L.off_diag = take(sh.mf ? sizeof(double) * npts : 0);
+    // multi-pass 3D mass intermediates (matfree_mp.cu)
+    const bool mp = sh.mf && sh.dim == 3;
+    const long long nfd = sh.g.nx;
+    L.off_mpT1 = take(mp ? sizeof(double) * sh.nvec * nq * nfd * nfd * sh.k : 0);
+    L.off_mpT2 = take(mp ? sizeof(double) * sh.nvec * nq * nq * nfd * sh.k : 0);
+    L.off_mpT3 = take(mp ? sizeof(double) * sh.nvec * nq * nq * nfd * sh.k : 0);
   }
   L.off_chain = take(sizeof(double) * 3 * sh.k * sh.nvec * sh.g.padded);
   for (int i = 0; i < 8; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
@@ -437,6 +444,7 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
     a.mf = 1; a.mfstiff = which; a.mfn = c->n; a.mfj0 = 0;
     a.mfW = which == 0 ? c->mfWM : c->mfWK; a.mfws = c->mfws;
     a.mfv = c->mftv; a.mfd = c->mftd;
+    if (which == 0 && !getenv("GA_MF_TILE")) { a.mpT1 = c->mpT1; a.mpT2 = c->mpT2; a.mpT3 = c->mpT3; }
   }
   a.mode = mode;
   // p = z + beta p as a separate elementwise pass (measured faster than forming
@@ -893,6 +901,11 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     ctx->mftv = (double*)(ws + L.off_mftab);
     ctx->mftd = ctx->mftv + nq * (sh.p + 1);
     ctx->diagM = (double*)(ws + L.off_diag);
+    if (sh.dim == 3) {
+      ctx->mpT1 = (double*)(ws + L.off_mpT1);
+      ctx->mpT2 = (double*)(ws + L.off_mpT2);
+      ctx->mpT3 = (double*)(ws + L.off_mpT3);
+    }
   }
   ctx->chain = (double*)(ws + L.off_chain);
   double** mv[8] = {&ctx->pred, &ctx->b, &ctx->x, &ctx->r, &ctx->z, &ctx->pv, &ctx->q, &ctx->pv1};

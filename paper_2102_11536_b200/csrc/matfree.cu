@@ -15,6 +15,10 @@ extern template void mf_launch_p<6>(const SpmvArgs&, cudaStream_t);
 extern template void mf_launch_p<7>(const SpmvArgs&, cudaStream_t);
 
 void launch_matfree(const SpmvArgs& a, cudaStream_t s) {
+  if (a.g.dim == 3 && !a.mfstiff && a.mpT1) {  // non-redundant multi-pass mass apply
+    launch_matfree_mp(a, s);
+    return;
+  }
   switch (a.p) {
     case 1: mf_launch_p<1>(a, s); break;
     case 2: mf_launch_p<2>(a, s); break;

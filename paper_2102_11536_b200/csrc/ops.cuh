@@ -46,10 +46,14 @@ struct SpmvArgs {
   // hguard rows (spmv_core.cuh spmv_block_half); not for the elastic (3x3-block) K
   int half;
   long long hguard;
+  // 3D matrix-free mass by the multi-pass non-redundant sum factorisation (matfree_mp.cu):
+  // intermediates T1 [c][n_q][nf][nf][k], T2 / T3 [c][n_q][n_q][nf][k]
+  double *mpT1, *mpT2, *mpT3;
 };
 void launch_spmv(const SpmvArgs& a, cudaStream_t s);
 // matrix-free variants (matfree.cu): the same contract as launch_spmv for a.mf = 1
 void launch_matfree(const SpmvArgs& a, cudaStream_t s);
+void launch_matfree_mp(const SpmvArgs& a, cudaStream_t s);  // 3D mass, multi-pass (a.mpT1 != null)
 // fixed-order sum of nb block partials + the PCG scalar step (SPMV_PQ / SPMV_TRUERES)
 void launch_spmv_fin(const SpmvArgs& a, unsigned int nb, cudaStream_t s);
 // diag(M) of the matrix-free mass operator on the single-patch grid, diag[npts]
