@@ -343,7 +343,14 @@ def run_ours(args, rank, world, local_rank):
             durs.append(e0.elapsed_time(e1))
         avg = sum(durs) / len(durs)
         kern[op] = dict(name=names[op], ms=avg, bytes=info_bytes[op])
-        if mfree and (op == 0 or (op == 1 and nc == 1)):
+        if mfree and op == 0 and cfg["dim"] == 3:
+            # multi-pass mass (matfree_mp.cu, HBM streams): Gauss weights once + per DoF and rhs the
+            # intermediates 2 + 2(p+1) + 2(p+1)^2 doubles
+            qd, p1 = cfg["n"] * (cfg["p"] + 1), cfg["p"] + 1
+            kern[op]["bytes"] = 8 * qd ** 3 + 8 * nc * cfg["k"] * info["npts"] * (2 + 2 * p1 + 2 * p1 * p1)
+            names[0] = "k_mp_* (M, matrix-free multi-pass)+p.q"
+            kern[op]["name"] = names[0]
+        elif mfree and (op == 0 or (op == 1 and nc == 1)):
             nfd = G[0]  # free bases per direction (single patch)
             qd = cfg["n"] * (cfg["p"] + 1)
             # compulsory bytes: Gauss-point data once (1 or d(d+1)/2 values), read x, write y

@@ -26,3 +26,4 @@ run --config c3 --p 2 --n 96 --k 3 --rho 1.0 --steps 10 --warmup 3
 run --config c3 --p 2 --n 96 --k 1 --rho 0.5 --steps 10 --warmup 3
 run --config c4 --steps 10 --warmup 3
 run --config c5 --steps 10 --warmup 3
+run --config e1 --steps 10 --warmup 3
