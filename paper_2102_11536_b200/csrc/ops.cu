@@ -605,6 +605,26 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
   }
 }
 
+// The z sweep of the streamed path with the PCG epilogue (after the plane-fused y/x sweeps).
+bool launch_line_sf_epi_z(const PrecArgs& a, cudaStream_t s) {
+  const GridDesc& g = a.g;
+  const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
+  const long long str[3] = {a.kk, (long long)g.nx * a.kk, (long long)g.nx * g.ny * a.kk};
+  const long long off = g.guard * a.kk;
+  LineArgs la;
+  memset(&la, 0, sizeof(la));
+  la.t = a.z + off; la.L = a.L[0][2]; la.len = bd[2]; la.es = str[2]; la.kk = a.kk; la.nvec = a.nvec;
+  la.sc = g.padded * a.kk;
+  la.na = bd[0]; la.sa = str[0];
+  la.nb = bd[1]; la.sb = str[1];
+  la.s = a.s[0];
+  la.x = a.x + off; la.r = a.r + off; la.p = a.p0 + off; la.q = a.q + off;
+  la.pcg = a.pcg; la.st = a.st; la.partial = a.partial; la.counter = a.counter;
+  la.maxit = a.maxit; la.update = a.update; la.cond = a.cond;
+  line_sf_dispatch(a.p, la, false, true, s);
+  return true;
+}
+
 void launch_precond(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
   const bool single = (a.npatch == 1 && a.t[0] == nullptr);

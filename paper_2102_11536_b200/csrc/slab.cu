@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "tile_core.cuh"
@@ -348,12 +349,177 @@ bool launch_line_slab(int p, const SlabArgs& a, bool pro, bool epi, cudaStream_t
   }
 }
 
+// Plane-fused y and x sweeps (3D, single patch, a whole xy-plane of the k right-hand sides in
+// shared memory): one CTA per (component, z-plane) loads the plane with the PCG prologue fused
+// (x += alpha p, r -= alpha q, t = s o r), runs the y-line solves (thread per (x, rhs) column)
+// and the x-line solves (thread per (y, rhs) row) on-chip, and writes the plane once; the z
+// sweep with the epilogue follows as a streamed kernel.  Row stride LDR = nx*kk + 1 (odd):
+// column walks and row walks are both conflict-free per half warp.
+template <int P>
+__global__ void __launch_bounds__(512) k_prec_plane(SlabArgs ay, SlabArgs ax, int nx, int ny, int nz) {
+  if (ay.st->status != 0) return;
+  count_launch(ay.st);
+  extern __shared__ double sm_pl[];
+  const int kk = ay.kk, rl = nx * kk, LDR = rl + 1;
+  double* Ly = sm_pl;                              // (ny + P + 1) x (P + 1)
+  double* Lx = Ly + (ny + P + 1) * (P + 1);        // (nx + P + 1) x (P + 1)
+  double* pl = Lx + (nx + P + 1) * (P + 1);        // [ny][LDR]
+  for (int i = threadIdx.x; i < (ny + P + 1) * (P + 1); i += blockDim.x) Ly[i] = __ldg(ay.L + i);
+  for (int i = threadIdx.x; i < (nx + P + 1) * (P + 1); i += blockDim.x) Lx[i] = __ldg(ax.L + i);
+  const int c = blockIdx.x / nz, z = blockIdx.x % nz;
+  const long long base = c * ay.sc + (long long)z * ny * rl;  // offset of (c, z, 0, 0, 0)
+  double al[KMAX];
+  bool upd = false;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) al[j] = 0.0;
+  if (ay.update && !ay.pcg->first) {
+    upd = true;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) al[j] = j < kk ? ay.pcg->alpha[j] : 0.0;
+  }
+  // ---- load with the prologue: rows of the plane are contiguous runs of rl doubles
+  for (int i = threadIdx.x; i < ny * rl; i += blockDim.x) {
+    const int y = i / rl, q = i - y * rl;
+    const long long o = base + i;
+    const int j = q % kk;
+    double aj = al[0];
+#pragma unroll
+    for (int jj = 1; jj < KMAX; ++jj) aj = (jj == j) ? al[jj] : aj;
+    double rv = ay.r[o];
+    if (upd) {
+      const double xv = ay.x[o], pv = ay.p[o], qv = ay.q[o];
+      ay.x[o] = fma(aj, pv, xv);
+      rv = fma(-aj, qv, rv);
+      ay.r[o] = rv;
+    }
+    pl[y * LDR + q] = rv * __ldg(ay.s + (o % ay.sc) / kk);
+  }
+  __syncthreads();
+  // ---- y lines: thread per column q = x*kk + j
+  for (int q = threadIdx.x; q < rl; q += blockDim.x) {
+    double* col = pl + q;
+    double ym[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) ym[u] = 0.0;
+    for (int i = 0; i < ny; ++i) {
+      const double* Li = Ly + i * (P + 1);
+      double v = col[i * LDR];
+#pragma unroll
+      for (int u = P; u >= 1; --u) v = fma(-Li[u], ym[u - 1], v);
+      v *= Li[0];
+#pragma unroll
+      for (int u = P - 1; u >= 1; --u) ym[u] = ym[u - 1];
+      ym[0] = v;
+      col[i * LDR] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < P; ++u) ym[u] = 0.0;
+    for (int i = ny - 1; i >= 0; --i) {
+      double v = col[i * LDR];
+#pragma unroll
+      for (int u = P; u >= 1; --u) v = fma(-Ly[(i + u) * (P + 1) + u], ym[u - 1], v);
+      v *= Ly[i * (P + 1)];
+#pragma unroll
+      for (int u = P - 1; u >= 1; --u) ym[u] = ym[u - 1];
+      ym[0] = v;
+      col[i * LDR] = v;
+    }
+  }
+  __syncthreads();
+  // ---- x lines: thread per (y, j)
+  for (int t = threadIdx.x; t < ny * kk; t += blockDim.x) {
+    const int y = t / kk, j = t - y * kk;
+    double* row = pl + y * LDR + j;
+    double ym[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) ym[u] = 0.0;
+    for (int i = 0; i < nx; ++i) {
+      const double* Li = Lx + i * (P + 1);
+      double v = row[i * kk];
+#pragma unroll
+      for (int u = P; u >= 1; --u) v = fma(-Li[u], ym[u - 1], v);
+      v *= Li[0];
+#pragma unroll
+      for (int u = P - 1; u >= 1; --u) ym[u] = ym[u - 1];
+      ym[0] = v;
+      row[i * kk] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < P; ++u) ym[u] = 0.0;
+    for (int i = nx - 1; i >= 0; --i) {
+      double v = row[i * kk];
+#pragma unroll
+      for (int u = P; u >= 1; --u) v = fma(-Lx[(i + u) * (P + 1) + u], ym[u - 1], v);
+      v *= Lx[i * (P + 1)];
+#pragma unroll
+      for (int u = P - 1; u >= 1; --u) ym[u] = ym[u - 1];
+      ym[0] = v;
+      row[i * kk] = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ny * rl; i += blockDim.x) {
+    const int y = i / rl, q = i - y * rl;
+    ay.t[base + i] = pl[y * LDR + q];
+  }
+}
+
+static size_t plane_smem(int nx, int ny, int p, int kk) {
+  return sizeof(double) * ((size_t)(ny + p + 1) * (p + 1) + (size_t)(nx + p + 1) * (p + 1) + (size_t)ny * (nx * kk + 1));
+}
+
+template <int P>
+static bool plane_go(const SlabArgs& ay, const SlabArgs& ax, int nx, int ny, int nz, int nvec, cudaStream_t s) {
+  const size_t sm = plane_smem(nx, ny, P, ay.kk);
+  if (sm > 227 * 1024) return false;
+  static size_t attr = 0;
+  if (sm > attr) {
+    if (cudaFuncSetAttribute(k_prec_plane<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+      return false;
+    attr = sm;
+  }
+  const int work = std::max(nx * ay.kk, ny * ay.kk);
+  const int threads = std::min(512, (work + 31) / 32 * 32);
+  k_prec_plane<P><<<(unsigned int)(nvec * nz), threads, sm, s>>>(ay, ax, nx, ny, nz);
+  return true;
+}
+
+bool launch_line_sf_epi_z(const PrecArgs& a, cudaStream_t s);  // ops.cu: streamed z sweep with the epilogue
+
+static bool launch_precond_plane(const PrecArgs& a, cudaStream_t s) {
+  const GridDesc& g = a.g;
+  const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
+  const long long kk = a.kk, off = g.guard * kk;
+  SlabArgs ay, ax;
+  memset(&ay, 0, sizeof(ay));
+  ay.t = a.z + off; ay.L = a.L[0][1]; ay.len = bd[1]; ay.kk = a.kk; ay.nvec = a.nvec; ay.sc = g.padded * kk;
+  ay.s = a.s[0]; ay.x = a.x + off; ay.r = a.r + off; ay.p = a.p0 + off; ay.q = a.q + off;
+  ay.pcg = a.pcg; ay.st = a.st; ay.update = a.update;
+  ax = ay;
+  ax.L = a.L[0][0]; ax.len = bd[0];
+  bool ok = false;
+  switch (a.p) {
+    case 1: ok = plane_go<1>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+    case 2: ok = plane_go<2>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+    case 3: ok = plane_go<3>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+    case 4: ok = plane_go<4>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+    case 5: ok = plane_go<5>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+    case 6: ok = plane_go<6>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+    default: ok = plane_go<7>(ay, ax, bd[0], bd[1], bd[2], a.nvec, s); break;
+  }
+  if (!ok) return false;
+  return launch_line_sf_epi_z(a, s);
+}
+
 // Host helper: one preconditioner application on a single-patch grid by slab
 // sweeps, directions y (PRO), x, z (EPI) as in the streamed path.
 bool launch_precond_slab(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
   if (g.dim != 3) return false;
   const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
+  static int plane_mode = -1;  // GA_PLANE=0 disables the plane-fused y/x sweeps
+  if (plane_mode < 0) { const char* e = getenv("GA_PLANE"); plane_mode = (e && *e == '0') ? 0 : 1; }
+  if (plane_mode && plane_smem(bd[0], bd[1], a.p, a.kk) <= 227 * 1024 && launch_precond_plane(a, s)) return true;
   // measured: the slab wins for short lines of one component (C3 p=4 n=96:
   // 137 vs 167 us per application); longer lines leave only ~4 warps per SM (one line set
   // per warp in shared memory) and the streamed sweeps are faster (n=128: 251 vs 309 us)

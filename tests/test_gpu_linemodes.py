@@ -1,6 +1,6 @@
 """GPU parity of every line-solve implementation of the Kronecker preconditioner
 (P:703-713): the chunked shared-memory tiles ('t'), the streamed thread-per-line
-sweeps ('s') and the shared-memory slabs ('b').  The automatic choice depends
+sweeps ('s'), the shared-memory slabs ('b') and the plane-fused y/x sweeps ('p').  The automatic choice depends
 on the grid size, so each mode is forced through GA_LINE_MODE in a fresh
 process (the mode is read once per process) on small 3D cases with ragged
 slabs (free lines not a multiple of 32 slots), k = 1..3, and the elastic
@@ -49,11 +49,12 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["t", "s", "b"])
+@pytest.mark.parametrize("mode", ["t", "s", "b", "p"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}_" + "_".join(f"{k}{v}" for k, v in c[1].items()))
 def test_line_mode_parity(mode, case):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"), cfg=(case[0], case[1]))
-    env = dict(os.environ, GA_LINE_MODE=mode)
+    # 'b': shared-memory slabs (plane fusion off); 'p': plane-fused y/x sweeps + streamed z
+    env = dict(os.environ, GA_LINE_MODE="b" if mode == "p" else mode, GA_PLANE="1" if mode == "p" else "0")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     r = json.loads(out.stdout.strip().splitlines()[-1])
