@@ -517,8 +517,11 @@ bool launch_precond_slab(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
   if (g.dim != 3) return false;
   const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
-  static int plane_mode = -1;  // GA_PLANE=0 disables the plane-fused y/x sweeps
-  if (plane_mode < 0) { const char* e = getenv("GA_PLANE"); plane_mode = (e && *e == '0') ? 0 : 1; }
+  // plane-fused y/x sweeps: opt-in (GA_PLANE=1).  Measured: 117 vs 136 us per
+  // application warm at C3 p=4 n=96 but equal cold and a slower step (one wave of n_f CTAs
+  // with one plane each is latency-bound), so the default keeps slabs / streamed sweeps
+  static int plane_mode = -1;
+  if (plane_mode < 0) { const char* e = getenv("GA_PLANE"); plane_mode = (e && *e == '1') ? 1 : 0; }
   if (plane_mode && plane_smem(bd[0], bd[1], a.p, a.kk) <= 227 * 1024 && launch_precond_plane(a, s)) return true;
   // measured: the slab wins for short lines of one component (C3 p=4 n=96:
   // 137 vs 167 us per application); longer lines leave only ~4 warps per SM (one line set
