@@ -518,7 +518,10 @@ static bool tile_multi_launch(TileMulti m, cudaStream_t s) {
     for (int r = 0; r < m.np; ++r) tot16 += ntiles_for(m.tl[r], 16);
     ST = tot16 >= 148 ? 16 : 8;
   }
-  while (ST > 8 && (C + 32 / ST - 1) / (32 / ST) > 16) ST >>= 1;
+  static int min_st = -1;  // GA_TILE_MINST: smallest slots per tile (8: up to 16 warps per CTA)
+  if (min_st < 0) { const char* e = getenv("GA_TILE_MINST"); min_st = e ? atoi(e) : 8; }
+  while (ST > min_st && (C + 32 / ST - 1) / (32 / ST) > 16) ST >>= 1;
+  if (min_st < 8) while (ST > min_st && (C + 32 / ST - 1) / (32 / ST) > 8) ST >>= 1;
   int t0 = 0;
   for (int r = 0; r < m.np; ++r) {
     m.tl[r].ST = ST;

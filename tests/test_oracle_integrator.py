@@ -164,3 +164,25 @@ def test_c1_instability_above_cfl(c1_disc):
         it = integrator.Integrator(d.M, d.K, 2, 0.5, dt)
         c = it.run(top, np.zeros_like(top), 400)
         assert (np.abs(c[0]).max() > 1e3) == grows
+
+
+def test_e1_closed_form_solves_the_wave_equation():
+    # E1 (reading G24): u = sin(10 pi x) sin(10 pi y)[cos + sin](10 sqrt2 pi t) must
+    # solve u_tt = Laplace(u) (omega = 1, f = 0) with u = 0 on the boundary of the unit square,
+    # and the second return value must be u_t; checked by centred differences at random points
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(0.0, 1.0, (50, 2))
+    h, ht = 1e-4, 1e-5
+    for t in (0.0, 0.037, 0.1):
+        u, ut = synth.e1_exact(pts, t)
+        up, _ = synth.e1_exact(pts, t + ht)
+        um, _ = synth.e1_exact(pts, t - ht)
+        np.testing.assert_allclose((up - um) / (2 * ht), ut, rtol=0, atol=1e-6 * np.abs(ut).max())
+        utt = (up - 2 * u + um) / ht ** 2
+        lap = 0.0
+        for dx in (np.array([h, 0.0]), np.array([0.0, h])):
+            lap = lap + (synth.e1_exact(pts + dx, t)[0] - 2 * u + synth.e1_exact(pts - dx, t)[0]) / h ** 2
+        scale = 200 * np.pi ** 2 * np.abs(u).max()
+        assert np.abs(utt - lap).max() < 1e-3 * scale
+    edge = np.array([[0.0, 0.3], [1.0, 0.7], [0.4, 0.0], [0.6, 1.0]])
+    assert np.abs(synth.e1_exact(edge, 0.05)[0]).max() < 1e-12
