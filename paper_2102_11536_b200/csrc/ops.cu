@@ -906,50 +906,62 @@ void launch_solve_end(PcgState* pcg, DevStatus* st, cudaStream_t s) { k_solve_en
 // ---------------------------------------------------------------------------
 // Stage update (reading R1): one thread per (component, DoF)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double taylor(const double* c, int m, int n3k, const double* f) {
+// T_m(c) = sum_{i=0}^{3k-1-m} tau^i / i! c_{m+i}, compile-time k: all registers
+template <int K>
+__device__ __forceinline__ double taylor_k(const double (&c)[3 * K], int m, const double* f) {
   double s = 0.0;
-  for (int i = n3k - 1 - m; i >= 0; --i) s = fma(f[i], c[m + i], s);
+#pragma unroll
+  for (int i = 3 * K - 1; i >= 0; --i)
+    if (i <= 3 * K - 1 - m) s = fma(f[i], c[m + i], s);
   return s;
 }
 
-template <bool STEP>
+template <bool STEP, int K>
 __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
+  constexpr int N3 = 3 * K;
   const bool dead = a.st->status != 0;
   if (!dead) count_launch(a.st);
   const GridDesc g = a.g;
-  const int k = a.k, n3 = 3 * a.k;
-  const long long tot = (long long)a.nvec * g.npts;
+  const long long npts = g.npts;
+  const long long vstride = (long long)a.nvec * g.padded;
   const long long estride = (long long)gridDim.x * blockDim.x;
+  double f[N3];
+#pragma unroll
+  for (int i = 0; i < N3; ++i) f[i] = a.f[i];
   double u2[1] = {0.0};
-  if (!dead) for (long long e = (long long)gtid(); e < tot; e += estride) {
-    const long long i = e % g.npts;
-    const int c = (int)(e / g.npts);
-    const long long vstride = (long long)a.nvec * g.padded;
-    const long long off = (long long)c * g.padded + g.guard + i;
-    double cc[3 * KMAX], nw[3 * KMAX];
-    for (int m = 0; m < n3; ++m) cc[m] = a.chain[m * vstride + off];
-    if (STEP) {
-      const long long yb = ((long long)c * g.padded + g.guard + i) * k;
-      for (int j = 0; j < k; ++j) {
-        const int d = 3 * j, v = 3 * j + 1, ac = 3 * j + 2;
-        const double Td = taylor(cc, d, n3, a.f), Tv = taylor(cc, v, n3, a.f), Ta = taylor(cc, ac, n3, a.f);
-        const double P = (a.ysol[yb + j] - Ta) / a.alpha[j];
-        nw[d] = fma(a.beta[j] * a.tau * a.tau, P, Td);
-        nw[v] = fma(a.gamma[j] * a.tau, P, Tv);
-        nw[ac] = Ta + P;
+  if (!dead)
+    for (int c = 0; c < a.nvec; ++c) {
+      const long long cb = (long long)c * g.padded + g.guard;
+      for (long long i = (long long)gtid(); i < npts; i += estride) {
+        const long long off = cb + i;
+        double cc[N3], nw[N3];
+#pragma unroll
+        for (int m = 0; m < N3; ++m) cc[m] = a.chain[m * vstride + off];
+        if (STEP) {
+          double y[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) y[j] = a.ysol[off * K + j];
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const int d = 3 * j, v = 3 * j + 1, ac = 3 * j + 2;
+            const double Td = taylor_k<K>(cc, d, f), Tv = taylor_k<K>(cc, v, f), Ta = taylor_k<K>(cc, ac, f);
+            const double P = (y[j] - Ta) / a.alpha[j];
+            nw[d] = fma(a.beta[j] * a.tau * a.tau, P, Td);
+            nw[v] = fma(a.gamma[j] * a.tau, P, Tv);
+            nw[ac] = Ta + P;
+          }
+#pragma unroll
+          for (int m = 0; m < N3; ++m) a.chain[m * vstride + off] = nw[m];
+        } else {
+#pragma unroll
+          for (int m = 0; m < N3; ++m) nw[m] = cc[m];
+        }
+        // predictors of the next step: s_j = T_disp(c) (j < k), s_k = c_{3k-3}
+#pragma unroll
+        for (int j = 0; j < K; ++j) a.pred[off * K + j] = (j < K - 1) ? taylor_k<K>(nw, 3 * j, f) : nw[3 * j];
+        u2[0] = fma(nw[0], nw[0], u2[0]);
       }
-      for (int m = 0; m < n3; ++m) a.chain[m * vstride + off] = nw[m];
-    } else {
-      for (int m = 0; m < n3; ++m) nw[m] = cc[m];
     }
-    // predictors of the next step: s_j = T_disp(c) (j < k), s_k = c_{3k-3}
-    const long long pb = ((long long)c * g.padded + g.guard + i) * k;
-    for (int j = 0; j < k; ++j) {
-      const int d = 3 * j;
-      a.pred[pb + j] = (j < k - 1) ? taylor(nw, d, n3, a.f) : nw[d];
-    }
-    u2[0] = fma(nw[0], nw[0], u2[0]);
-  }
   if (dead || !STEP) return;
   double out[1];
   if (reduce_last_block<1>(u2, a.partial, a.counter, out)) {
@@ -962,14 +974,19 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
     }
   }
 }
-void launch_stage(const StageArgs& a, cudaStream_t s) {
-  const long long tot = (long long)a.nvec * a.g.npts;
-  k_stage<true><<<red_grid(tot), NTHREADS, 0, s>>>(a);
+
+template <bool STEP>
+static void stage_go(const StageArgs& a, cudaStream_t s) {
+  const unsigned int nb = red_grid(a.g.npts);
+  switch (a.k) {
+    case 1: k_stage<STEP, 1><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 2: k_stage<STEP, 2><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 3: k_stage<STEP, 3><<<nb, NTHREADS, 0, s>>>(a); break;
+    default: k_stage<STEP, 4><<<nb, NTHREADS, 0, s>>>(a); break;
+  }
 }
-void launch_predict(const StageArgs& a, cudaStream_t s) {
-  const long long tot = (long long)a.nvec * a.g.npts;
-  k_stage<false><<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
-}
+void launch_stage(const StageArgs& a, cudaStream_t s) { stage_go<true>(a, s); }
+void launch_predict(const StageArgs& a, cudaStream_t s) { stage_go<false>(a, s); }
 
 // ---------------------------------------------------------------------------
 // Packing / copies / small reductions
