@@ -62,6 +62,44 @@ __global__ void __launch_bounds__(NTHREADS) k_xr_prec_in(PrecArgs a) {
   }
 }
 
+// multi-patch prologue fused with the gather (additive Schwarz): one thread per (grid
+// point, rhs) applies x += alpha p, r -= alpha q once, then writes s_r o r into the box of every
+// patch that contains the point (interface points belong to 2-4 boxes); 32-bit index math
+template <int KK>
+__global__ void __launch_bounds__(NTHREADS) k_xr_gather(PrecArgs a) {
+  if (a.st->status != 0) return;
+  count_launch(a.st);
+  const GridDesc g = a.g;
+  const int npts = (int)g.npts;
+  const int tot = a.nvec * npts * KK;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const int j = e % KK;
+  const int ci = e / KK;
+  const int c = ci / npts, i = ci - c * npts;
+  const long long idx = ((long long)c * g.padded + g.guard + i) * KK + j;
+  double r = a.r[idx];
+  if (a.update && !a.pcg->first) {
+    const double al = a.pcg->alpha[j];
+    const double* pp = (a.pcg->iter & 1) ? a.p1 : a.p0;
+    if (al != 0.0) {
+      a.x[idx] = fma(al, pp[idx], a.x[idx]);
+      r = fma(-al, a.q[idx], r);
+      a.r[idx] = r;
+    }
+  }
+  const int ix = i % g.nx, iyz = i / g.nx;
+  const int iy = iyz % g.ny, iz = iyz / g.ny;
+  for (int pr = 0; pr < a.npatch; ++pr) {
+    const int lx = ix - a.lo[pr][0], ly = iy - a.lo[pr][1], lz = iz - a.lo[pr][2];
+    const int bx = a.bd[pr][0], by = a.bd[pr][1], bz = a.bd[pr][2];
+    if (lx < 0 || ly < 0 || lz < 0 || lx >= bx || ly >= by || lz >= bz) continue;
+    const int bi = lx + bx * (ly + by * lz);
+    const long long nbox = (long long)bx * by * bz;
+    a.t[pr][((long long)c * nbox + bi) * KK + j] = a.s[pr][bi] * r;
+  }
+}
+
 // multi-patch gather: t_r = s_r o R_r r on the box of patch r
 // all patches in one launch: element ranges of the patches are consecutive
 __global__ void __launch_bounds__(NTHREADS) k_prec_gather_all(PrecArgs a) {
@@ -565,9 +603,10 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
   double v[2 * KK];
 #pragma unroll
   for (int j = 0; j < 2 * KK; ++j) v[j] = 0.0;
+  const int npts = (int)g.npts;  // < 2^31 grid points (checked by the launcher)
   if (!dead) for (long long e = (long long)gtid(); e < tot; e += estride) {
-    const long long i = e % g.npts;
-    const int c = (int)(e / g.npts);
+    const int c = (int)(e / npts);
+    const int i = (int)e - c * npts;
     const long long base = ((long long)c * g.padded + g.guard + i) * KK;
     double z[KK];
     if (a.npatch == 1 && a.t[0] == nullptr) {
@@ -577,14 +616,15 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
     } else {
 #pragma unroll
       for (int j = 0; j < KK; ++j) z[j] = 0.0;
-      const int ix = (int)(i % g.nx), iy = (int)((i / g.nx) % g.ny), iz = (int)(i / ((long long)g.nx * g.ny));
+      const int iyz = i / g.nx, ix = i - iyz * g.nx;
+      const int iz = iyz / g.ny, iy = iyz - iz * g.ny;
       const bool free_pt = a.mask == nullptr || a.mask[i];
       if (free_pt) {
         for (int pr = 0; pr < a.npatch; ++pr) {
           const int lx = ix - a.lo[pr][0], ly = iy - a.lo[pr][1], lz = iz - a.lo[pr][2];
           if (lx < 0 || ly < 0 || lz < 0 || lx >= a.bd[pr][0] || ly >= a.bd[pr][1] || lz >= a.bd[pr][2]) continue;
           const long long nbox = (long long)a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2];
-          const long long bi = lx + (long long)a.bd[pr][0] * (ly + (long long)a.bd[pr][1] * lz);
+          const int bi = lx + a.bd[pr][0] * (ly + a.bd[pr][1] * lz);
           const double sv = a.s[pr][bi];
 #pragma unroll
           for (int j = 0; j < KK; ++j) z[j] = fma(sv, a.t[pr][((long long)c * nbox + bi) * KK + j], z[j]);
@@ -709,15 +749,26 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     if (ok) return;
   }
   // general path (multi-patch / very long lines)
-  {
+  const bool batched = !single && !stream;
+  if (batched && a.nvec * g.npts * a.kk < (1LL << 31)) {
+    // batched Schwarz: prologue + gather in one pass, then one tile launch per direction
+    const unsigned int nbg = (unsigned int)((a.nvec * g.npts * a.kk + NTHREADS - 1) / NTHREADS);
+    switch (a.kk) {
+      case 1: k_xr_gather<1><<<nbg, NTHREADS, 0, s>>>(a); break;
+      case 2: k_xr_gather<2><<<nbg, NTHREADS, 0, s>>>(a); break;
+      case 3: k_xr_gather<3><<<nbg, NTHREADS, 0, s>>>(a); break;
+      default: k_xr_gather<4><<<nbg, NTHREADS, 0, s>>>(a); break;
+    }
+  } else {
     const long long tot = (long long)a.nvec * g.npts * a.kk;
     k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+    if (batched) {
+      long long tb = 0;
+      for (int pr = 0; pr < a.npatch; ++pr) tb += (long long)a.nvec * a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2] * a.kk;
+      k_prec_gather_all<<<(unsigned int)((tb + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+    }
   }
-  if (!single && !stream) {
-    // batched Schwarz: one gather and one tile launch per direction for all patches
-    long long tot = 0;
-    for (int pr = 0; pr < a.npatch; ++pr) tot += (long long)a.nvec * a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2] * a.kk;
-    k_prec_gather_all<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+  if (batched) {
     bool ok = true;
     for (int d = 0; d < g.dim && ok; ++d) {
       TileMulti m;
@@ -823,9 +874,10 @@ __global__ void __launch_bounds__(NTHREADS) k_init_from_b(VecArgs a) {
   double v[KK];
 #pragma unroll
   for (int j = 0; j < KK; ++j) v[j] = 0.0;
+  const int npts = (int)g.npts;  // < 2^31 grid points (checked by the launcher)
   if (!dead) for (long long e = (long long)gtid(); e < tot; e += estride) {
-    const long long i = e % g.npts;
-    const int c = (int)(e / g.npts);
+    const int c = (int)(e / npts);
+    const int i = (int)e - c * npts;
     const long long base = ((long long)c * g.padded + g.guard + i) * KK;
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
