@@ -648,6 +648,8 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
   }
 }
 
+bool launch_xslab(const PrecArgs& a, cudaStream_t s);  // slab.cu
+
 // The z sweep of the streamed path with the PCG epilogue (after the plane-fused y/x sweeps).
 bool launch_line_sf_epi_z(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
@@ -696,8 +698,11 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     const long long off = g.guard * a.kk;
     int order[3] = {1, 0, 2};
     if (g.dim == 2) { order[0] = 1; order[1] = 0; }
+    static int xslab = -1;  // GA_XSLAB=1: the middle (x) sweep as a shared-memory slab (coalesced x lines)
+    if (xslab < 0) { const char* e = getenv("GA_XSLAB"); xslab = (e && *e == '1') ? 1 : 0; }
     for (int k = 0; k < g.dim; ++k) {
       const int d = order[k];
+      if (xslab && d == 0 && g.dim == 3 && k != 0 && k != g.dim - 1 && launch_xslab(a, s)) continue;
       LineArgs la;
       memset(&la, 0, sizeof(la));
       la.t = a.z + off; la.L = a.L[0][d]; la.len = bd[d]; la.es = str[d]; la.kk = a.kk; la.nvec = a.nvec;

@@ -511,6 +511,20 @@ static bool launch_precond_plane(const PrecArgs& a, cudaStream_t s) {
   return launch_line_sf_epi_z(a, s);
 }
 
+// The x sweep alone as a slab (no prologue / epilogue), between streamed y and z sweeps.
+bool launch_xslab(const PrecArgs& a, cudaStream_t s) {
+  const GridDesc& g = a.g;
+  if (!slab_supported(a.bd[0][0], a.p, a.kk)) return false;
+  const long long kk = a.kk, off = g.guard * kk;
+  SlabArgs sa;
+  memset(&sa, 0, sizeof(sa));
+  sa.t = a.z + off; sa.L = a.L[0][0]; sa.len = a.bd[0][0]; sa.kk = a.kk; sa.nvec = a.nvec;
+  sa.sc = g.padded * kk; sa.s = a.s[0];
+  sa.pcg = a.pcg; sa.st = a.st; sa.partial = a.partial; sa.counter = a.counter;
+  sa.dirx = 1; sa.es = kk; sa.nrow = (long long)g.ny * g.nz; sa.srow = (long long)g.nx * kk;
+  return launch_line_slab(a.p, sa, false, false, s);
+}
+
 // Host helper: one preconditioner application on a single-patch grid by slab
 // sweeps, directions y (PRO), x, z (EPI) as in the streamed path.
 bool launch_precond_slab(const PrecArgs& a, cudaStream_t s) {
