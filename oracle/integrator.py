@@ -16,7 +16,12 @@ SURVEY.md §8c G1 for the K-term of blocks j < k; F = C = 0):
 All k blocks read only old-step data.
 
 Initial chain (P:119-121, P:155-162 generalised, reading R3):
-  c_0 = U_0, c_1 = V_0, c_m = M^{-1}(-K c_{m-2}), m = 2 .. 3k-1."""
+  c_0 = U_0, c_1 = V_0, c_m = M^{-1}(-K c_{m-2}), m = 2 .. 3k-1.
+
+Forcing (eq:ho1 P:398-404): block j's right-hand side is
+F^{(3j-3)}(t_n + alpha_fj tau) - K s_j, and the initial chain is
+c_m = M^{-1}(F^{(m-2)}(t_0) - K c_{m-2}) (the ODE differentiated m-2 times at t_0).
+Here F(t) = G h(t) with h a sum of sinusoids, whose derivatives are closed form."""
 from __future__ import annotations
 
 import math
@@ -54,22 +59,43 @@ def taylor(c, m: int, tau: float):
     return out
 
 
-def initial_chain(u0, v0, k: int, solve, Kop):
-    """c_0 = U_0, c_1 = V_0, c_m = M^{-1}(-K c_{m-2}) for m = 2..3k-1."""
+class Forcing:
+    """F(t) = G h(t), h(t) = sum_i a_i cos(w_i t + phi_i); F^{(m)}(t) = G h^{(m)}(t) with
+    h^{(m)}(t) = sum_i a_i w_i^m cos(w_i t + phi_i + m pi / 2)."""
+
+    def __init__(self, G, terms):
+        self.G = np.asarray(G, dtype=np.float64)
+        self.terms = [(float(a), float(w), float(ph)) for a, w, ph in terms]
+
+    def h(self, m: int, t: float) -> float:
+        return sum(a * w ** m * math.cos(w * t + ph + m * math.pi / 2) for a, w, ph in self.terms)
+
+    def __call__(self, m: int, t: float):
+        return self.h(m, t) * self.G
+
+
+def initial_chain(u0, v0, k: int, solve, Kop, F=None, t0: float = 0.0):
+    """c_0 = U_0, c_1 = V_0, c_m = M^{-1}(F^{(m-2)}(t_0) - K c_{m-2}) for m = 2..3k-1."""
     c = [np.array(u0, dtype=np.float64), np.array(v0, dtype=np.float64)]
     for m in range(2, 3 * k):
-        c.append(solve(-(Kop @ c[m - 2])))
+        rhs = -(Kop @ c[m - 2])
+        if F is not None:
+            rhs = rhs + F(m - 2, t0)
+        c.append(solve(rhs))
     return c
 
 
-def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop):
-    """One explicit step of the order-2k scheme; returns the new chain."""
+def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop, F=None, t: float = 0.0, alpha_f=None):
+    """One explicit step of the order-2k scheme from time t; returns the new chain."""
     new = [None] * (3 * k)
     for j in range(1, k + 1):
         d, v, a = 3 * j - 3, 3 * j - 2, 3 * j - 1
         Td, Tv, Ta = taylor(c, d, tau), taylor(c, v, tau), taylor(c, a, tau)
         s = Td if j < k else c[d]
-        y = solve(-(Kop @ s))
+        rhs = -(Kop @ s)
+        if F is not None:  # F^{(3j-3)} at t_n + alpha_fj tau (eq:ho1)
+            rhs = rhs + F(3 * j - 3, t + alpha_f[j - 1] * tau)
+        y = solve(rhs)
         P = (y - Ta) / alpha[j - 1]
         new[d] = Td + beta[j - 1] * tau * tau * P
         new[v] = Tv + gamma[j - 1] * tau * P
@@ -80,17 +106,23 @@ def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop):
 class Integrator:
     """Convenience driver: M, K (free-DoF sparse matrices), k, rho, dt."""
 
-    def __init__(self, M, K, k: int, rho: float, dt: float, param_set: int = 0, solver=None):
+    def __init__(self, M, K, k: int, rho: float, dt: float, param_set: int = 0, solver=None, forcing=None,
+                 t0: float = 0.0):
         self.M, self.K = sp.csr_matrix(M), sp.csr_matrix(K)
         self.k, self.dt = k, dt
         self.alpha, self.beta, self.gamma, self.alpha_f = scheme_params(k, rho, param_set)
         self.solve = solver if solver is not None else DirectMassSolver(self.M)
+        self.F, self.t0, self.n = forcing, t0, 0
 
     def init(self, u0, v0):
-        return initial_chain(u0, v0, self.k, self.solve, self.K)
+        self.n = 0
+        return initial_chain(u0, v0, self.k, self.solve, self.K, self.F, self.t0)
 
     def step(self, c):
-        return step(c, self.k, self.dt, self.alpha, self.beta, self.gamma, self.solve, self.K)
+        out = step(c, self.k, self.dt, self.alpha, self.beta, self.gamma, self.solve, self.K, self.F,
+                   self.t0 + self.n * self.dt, self.alpha_f)
+        self.n += 1
+        return out
 
     def run(self, u0, v0, nsteps: int, chain=None):
         c = self.init(u0, v0) if chain is None else chain

@@ -186,3 +186,35 @@ def test_e1_closed_form_solves_the_wave_equation():
         assert np.abs(utt - lap).max() < 1e-3 * scale
     edge = np.array([[0.0, 0.3], [1.0, 0.7], [0.4, 0.0], [0.6, 1.0]])
     assert np.abs(synth.e1_exact(edge, 0.05)[0]).max() < 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_forced_scalar_ode_order_2k(k):
+    # Forcing (eq:ho1, F^{(3j-3)} at t_n + alpha_fj tau; initial chain with F^{(m-2)}(0)):
+    # u'' + w^2 u = cos(2t) + 0.5 cos(3t + 0.4), u(0) = 1, v(0) = 0.3, closed-form solution.
+    # Evaluating the forcing at t_n instead of t_n + alpha_f tau (or dropping its derivatives
+    # from the chain) breaks order 2k for k >= 2 -- this pins the reading.
+    w, T, rho = 1.3, 4.0, 0.5
+    terms = [(1.0, 2.0, 0.0), (0.5, 3.0, 0.4)]
+    part = lambda t, d=0: sum(a / (w * w - om * om) * om ** d * math.cos(om * t + ph + d * math.pi / 2)
+                              for a, om, ph in terms)
+    A = 1.0 - part(0.0)
+    B = (0.3 - part(0.0, 1)) / w
+    ue = lambda t: A * math.cos(w * t) + B * math.sin(w * t) + part(t)
+    ve = lambda t: -A * w * math.sin(w * t) + B * w * math.cos(w * t) + part(t, 1)
+    F = integrator.Forcing(np.array([1.0]), terms)
+    errs_u, errs_v = [], []
+    taus = [0.2 / 2 ** i for i in range(5)] if k < 3 else [0.4 / 2 ** i for i in range(4)]
+    for tau in taus:
+        it = integrator.Integrator(np.eye(1), np.array([[w * w]]), k, rho, tau, solver=lambda b: b, forcing=F)
+        c = it.init(np.array([1.0]), np.array([0.3]))
+        eu = ev = 0.0
+        for n in range(1, int(round(T / tau)) + 1):
+            c = it.step(c)
+            eu = max(eu, abs(c[0][0] - ue(n * tau)))
+            ev = max(ev, abs(c[1][0] - ve(n * tau)))
+        errs_u.append(eu)
+        errs_v.append(ev)
+    ou, ov = _orders(errs_u), _orders(errs_v)
+    assert ou[-1] > 2 * k - 0.35, (ou, errs_u)
+    assert ov[-1] > 2 * k - 0.35, (ov, errs_v)
