@@ -148,6 +148,17 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
  * sides are skipped).  d_v0 may be NULL (V0 = 0).  Resets stats. */
 ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void* stream);
 
+/* Forcing F(x, t) = G(x) h(t) with h(t) = sum_{i<nterms} amp_i cos(omega_i t + phase_i)
+ * (eq:ho1 P:398-404): block j's right-hand side becomes
+ * F^{(3j-3)}(t_n + alpha_fj dt) - K s_j, and the initial chain of ga_set_state
+ * c_m = M^{-1}(F^{(m-2)}(t0) - K c_{m-2}); t_n = t0 + n dt with n the steps since
+ * ga_set_state.  d_G: device free-DoF vector of the load integrals int g B_i (layout as
+ * ga_set_state's u0), copied; NULL (or nterms = 0) removes the forcing.  1 <= nterms <= 8,
+ * amp/omega/phase: host arrays, copied.  Call before ga_set_state for a forced initial
+ * chain.  SYNCHRONIZES stream (the step graphs are re-captured).  GA_ERR_ARG on bad terms. */
+ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const double* amp, const double* omega,
+                         const double* phase, double t0, void* stream);
+
 /* Advance nsteps explicit steps.  Asynchronous; a device-side
  * failure stops further steps and is reported by ga_get_stats. */
 ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream);

@@ -80,6 +80,12 @@ struct ga_ctx {
   bool half = false;     // half-symmetric stencils (offsets o >= 0, zero guard of g.guard rows)
   double *mfWM = nullptr, *mfWK = nullptr, *mftv = nullptr, *mftd = nullptr, *diagM = nullptr;
   double *mpT1 = nullptr, *mpT2 = nullptr, *mpT3 = nullptr;  // 3D multi-pass mass intermediates
+  // forcing F = G h(t) (ga_set_forcing): grid vector, device slot table, host parameters
+  double* forceG = nullptr;
+  ForceSlots* fslots = nullptr;
+  bool forcing = false;
+  int fnterms = 0;
+  double famp[FMAXTERMS], fomega[FMAXTERMS], fphase[FMAXTERMS], ft0 = 0.0;
   long long mfws = 0;    // Gauss points (n(p+1))^dim
   long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
 };
@@ -104,7 +110,7 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t off_coefM, off_coefK, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
-      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3;
+      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
 };
@@ -344,6 +350,8 @@ Layout make_layout(const Shape& sh) {
   L.off_partial = take(sizeof(double) * 2 * KMAX * maxblocks);
   L.off_counter = take(sizeof(unsigned int) * 16);
   L.off_dscal = take(sizeof(double) * 16);
+  L.off_forceG = take(sizeof(double) * sh.nvec * sh.g.padded);
+  L.off_fslots = take(sizeof(ForceSlots));
   for (size_t r = 0; r < sh.prec.size(); ++r) {
     const PrecPatch& pp = sh.prec[r];
     long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
@@ -483,6 +491,16 @@ StageArgs stage_args(ga_ctx* c) {
   return a;
 }
 
+ForceArgs force_args(ga_ctx* c) {
+  ForceArgs a;
+  memset(&a, 0, sizeof(a));
+  a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.nterms = c->fnterms;
+  for (int i = 0; i < c->fnterms; ++i) { a.amp[i] = c->famp[i]; a.omega[i] = c->fomega[i]; a.phase[i] = c->fphase[i]; }
+  a.t0 = c->ft0; a.dt = c->d.dt;
+  a.G = c->forceG; a.b = c->b; a.slots = c->fslots; a.st = c->st;
+  return a;
+}
+
 PersistArgs persist_args(ga_ctx* ctx) {
   PersistArgs A;
   memset(&A, 0, sizeof(A));
@@ -554,6 +572,7 @@ enum GraphKind { GK_STEP = 0, GK_SOLVEK = 1, GK_SOLVEB = 2 };
 ga_status build_graph(ga_ctx* ctx, cudaStream_t s, GraphKind kind, cudaGraph_t* gout, cudaGraphExec_t* eout) {
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
   if (kind != GK_SOLVEB) launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->b, SPMV_NEGB), s);
+  if (kind != GK_SOLVEB && ctx->forcing) launch_add_forcing(force_args(ctx), s);
   ga_status rc = capture_solve(ctx, s);
   if (rc == GA_OK && kind == GK_STEP) launch_stage(stage_args(ctx), s);
   cudaGraph_t g = nullptr;
@@ -785,6 +804,7 @@ ga_status run_pcg_loop_direct(ga_ctx* ctx, cudaStream_t s) {
 
 ga_status run_direct(ga_ctx* ctx, GraphKind kind, cudaStream_t s) {
   if (kind != GK_SOLVEB) launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->b, SPMV_NEGB), s);
+  if (kind != GK_SOLVEB && ctx->forcing) launch_add_forcing(force_args(ctx), s);
   dbg(ctx, s, "negb");
   if (ctx->persist) {
     if (!launch_pcg_persist(persist_args(ctx), s)) {
@@ -918,6 +938,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->partial = (double*)(ws + L.off_partial);
   ctx->counter = (unsigned int*)(ws + L.off_counter);
   ctx->dscal = (double*)(ws + L.off_dscal);
+  ctx->forceG = (double*)(ws + L.off_forceG);
+  ctx->fslots = (ForceSlots*)(ws + L.off_fslots);
 #define CKD(call)                           \
   do {                                      \
     cudaError_t e_ = (call);                \
@@ -1054,7 +1076,21 @@ static ga_status check_ctx(ga_ctx* ctx) {
   return GA_OK;
 }
 
+// step slot table: block j (slot j-1) takes F^{(3j-3)} at t_n + alpha_fj dt (eq:ho1)
+static ga_status set_step_slots(ga_ctx* ctx, cudaStream_t s) {
+  if (!ctx->forcing) return GA_OK;
+  ForceSlots fs;
+  memset(&fs, 0, sizeof(fs));
+  for (int j = 0; j < ctx->k; ++j) { fs.active[j] = 1; fs.order[j] = 3 * j; fs.toff[j] = ctx->alpha_f[j] * ctx->d.dt; }
+  CK(cudaMemcpyAsync(ctx->fslots, &fs, sizeof(fs), cudaMemcpyHostToDevice, s));
+  return GA_OK;
+}
+
 static ga_status set_predictors_and_norm(ga_ctx* ctx, cudaStream_t s) {
+  {
+    ga_status rc = set_step_slots(ctx, s);
+    if (rc != GA_OK) return rc;
+  }
   launch_predict(stage_args(ctx), s);
   // ||U0||^2 for the instability detector
   launch_dot(ctx->g, ctx->nvec, 1, ctx->chain, ctx->chain, &ctx->st->u0norm2, ctx->partial, ctx->counter, s);
@@ -1080,6 +1116,13 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
     int src[KMAX] = {-1, -1, -1, -1}, dst[KMAX] = {-1, -1, -1, -1};
     for (int j = 0; j < batch; ++j)
       if (m0 + j <= 3 * k - 1) { src[j] = m0 + j - 2; dst[j] = m0 + j; }
+    if (ctx->forcing) {  // c_m = M^{-1}(F^{(m-2)}(t0) - K c_{m-2}) (eq:ho1 differentiated)
+      ForceSlots fs;
+      memset(&fs, 0, sizeof(fs));
+      for (int j = 0; j < batch; ++j)
+        if (dst[j] >= 0) { fs.active[j] = 1; fs.order[j] = dst[j] - 2; fs.toff[j] = 0.0; }
+      CK(cudaMemcpyAsync(ctx->fslots, &fs, sizeof(fs), cudaMemcpyHostToDevice, s));
+    }
     launch_pack(ctx->g, nvec, k, ctx->chain, src, ctx->pred, ctx->st, s);
     rc = run_kind(ctx, GK_SOLVEK, s);
     if (rc != GA_OK) return rc;
@@ -1087,6 +1130,48 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
     CK(cudaGetLastError());
   }
   return set_predictors_and_norm(ctx, s);
+}
+
+ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const double* amp, const double* omega,
+                         const double* phase, double t0, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool on = d_G != nullptr && nterms > 0;
+  if (on && (nterms > FMAXTERMS || !amp || !omega || !phase)) {
+    seterr(ctx, "forcing: 1..8 terms with amp, omega and phase arrays required");
+    return GA_ERR_ARG;
+  }
+  for (int i = 0; on && i < nterms; ++i)
+    if (!std::isfinite(amp[i]) || !std::isfinite(omega[i]) || !std::isfinite(phase[i])) {
+      seterr(ctx, "forcing: non-finite term");
+      return GA_ERR_ARG;
+    }
+  ctx->forcing = on;
+  ctx->fnterms = on ? nterms : 0;
+  ctx->ft0 = t0;
+  for (int i = 0; i < ctx->fnterms; ++i) { ctx->famp[i] = amp[i]; ctx->fomega[i] = omega[i]; ctx->fphase[i] = phase[i]; }
+  if (on) {
+    CK(cudaMemsetAsync(ctx->forceG, 0, sizeof(double) * ctx->nvec * ctx->g.padded, s));
+    launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_G, ctx->forceG, 1, 0, ctx->st, s);
+    CK(cudaGetLastError());
+  }
+  // the captured graphs carry the forcing kernel (and its parameters): rebuild them
+  CK(cudaStreamSynchronize(s));
+  if (!ctx->nograph) {
+    cudaGraphExec_t* ex[3] = {&ctx->g_step, &ctx->g_solveK, &ctx->g_solveB};
+    cudaGraph_t* gr[3] = {&ctx->gr_step, &ctx->gr_solveK, &ctx->gr_solveB};
+    for (int i = 0; i < 3; ++i) {
+      if (*ex[i]) cudaGraphExecDestroy(*ex[i]);
+      if (*gr[i]) cudaGraphDestroy(*gr[i]);
+      *ex[i] = nullptr; *gr[i] = nullptr;
+    }
+    rc = build_graph(ctx, ctx->cap, GK_STEP, &ctx->gr_step, &ctx->g_step);
+    if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEK, &ctx->gr_solveK, &ctx->g_solveK);
+    if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEB, &ctx->gr_solveB, &ctx->g_solveB);
+    if (rc != GA_OK) return rc;
+  }
+  return set_step_slots(ctx, s);
 }
 
 ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream) {

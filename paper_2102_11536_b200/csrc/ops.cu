@@ -1032,6 +1032,44 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
   }
 }
 
+template <int KK>
+__global__ void __launch_bounds__(NTHREADS) k_add_forcing(ForceArgs a) {
+  if (a.st->status != 0) return;
+  count_launch(const_cast<DevStatus*>(a.st));
+  const GridDesc g = a.g;
+  // h^{(m)}(t) per slot, identical in every thread (computed redundantly: a few terms)
+  double hj[KK];
+  const double tn = a.t0 + (double)a.st->steps * a.dt;
+#pragma unroll
+  for (int j = 0; j < KK; ++j) {
+    double h = 0.0;
+    if (a.slots->active[j]) {
+      const int m = a.slots->order[j];
+      const double t = tn + a.slots->toff[j];
+      for (int i = 0; i < a.nterms; ++i) h += a.amp[i] * pow(a.omega[i], (double)m) * cos(a.omega[i] * t + a.phase[i] + m * 1.5707963267948966);
+    }
+    hj[j] = h;
+  }
+  const long long tot = (long long)a.nvec * g.npts;
+  for (long long e = (long long)gtid(); e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / g.npts, i = e - c * g.npts;
+    const long long gi = c * g.padded + g.guard + i;
+    const double G = a.G[gi];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) a.b[gi * KK + j] = fma(hj[j], G, a.b[gi * KK + j]);
+  }
+}
+
+void launch_add_forcing(const ForceArgs& a, cudaStream_t s) {
+  const unsigned int nb = red_grid((long long)a.nvec * a.g.npts);
+  switch (a.kk) {
+    case 1: k_add_forcing<1><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 2: k_add_forcing<2><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 3: k_add_forcing<3><<<nb, NTHREADS, 0, s>>>(a); break;
+    default: k_add_forcing<4><<<nb, NTHREADS, 0, s>>>(a); break;
+  }
+}
+
 template <bool STEP>
 static void stage_go(const StageArgs& a, cudaStream_t s) {
   const unsigned int nb = red_grid(a.g.npts);

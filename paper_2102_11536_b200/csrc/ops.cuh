@@ -121,6 +121,28 @@ struct StageArgs {
 };
 void launch_stage(const StageArgs& a, cudaStream_t s);
 
+// Forcing F(x, t) = G(x) h(t), h(t) = sum_i amp_i cos(omega_i t + phase_i) (eq:ho1):
+// b_j += h^{(order_j)}(t0 + steps dt + toff_j) G for the active right-hand-side slots j.  The slot
+// table lives on the device (written before each solve set: the initial chain uses orders m-2 at
+// t0, the step orders 3j at t_n + alpha_fj dt), so the captured graphs need no rebuild.
+constexpr int FMAXTERMS = 8;
+struct ForceSlots {
+  int active[KMAX];
+  int order[KMAX];
+  double toff[KMAX];
+};
+struct ForceArgs {
+  GridDesc g;
+  int nvec, kk, nterms;
+  double amp[FMAXTERMS], omega[FMAXTERMS], phase[FMAXTERMS];
+  double t0, dt;
+  const double* G;           // grid vector [c][guard | npts | guard]
+  double* b;                 // MV [c][guard | npts | guard][kk]
+  const ForceSlots* slots;   // device
+  const DevStatus* st;       // st->steps: completed steps since ga_set_state
+};
+void launch_add_forcing(const ForceArgs& a, cudaStream_t s);
+
 // Predictors from the chain (after set_state / set_chain), same rule as the stage kernel.
 void launch_predict(const StageArgs& a, cudaStream_t s);
 

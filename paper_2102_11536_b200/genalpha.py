@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
                 -4: "GA_ERR_CONFORMITY", -5: "GA_ERR_NOCONV", -6: "GA_ERR_UNSTABLE",
                 -7: "GA_ERR_CUDA", -8: "GA_ERR_OOM"}
 
-EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_advance", "ga_get_state",
+EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
             "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_operator_mode", "ga_destroy",
             "ga_last_error"]
@@ -66,6 +66,7 @@ def _load():
         "ga_create": (c_int, [D, c_void_p, c_size_t, c_void_p, c_size_t, c_void_p, POINTER(c_void_p)]),
         "ga_set_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
         "ga_advance": (c_int, [c_void_p, c_int, c_void_p]),
+        "ga_set_forcing": (c_int, [c_void_p, c_void_p, c_int, P, P, P, c_double, c_void_p]),
         "ga_get_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
         "ga_get_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
         "ga_set_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
@@ -179,6 +180,14 @@ class Context:
 
     def set_state(self, u0, v0=None):
         _check(lib.ga_set_state(self.ctx, _ptr(u0), _ptr(v0) if v0 is not None else None, self._s()), self.ctx)
+
+    def set_forcing(self, G=None, terms=(), t0=0.0):
+        """F(x, t) = G h(t), h(t) = sum a cos(w t + phi) for (a, w, phi) in terms; G: free-DoF
+        tensor of the load integrals (None removes the forcing).  Call before set_state."""
+        n = len(terms) if G is not None else 0
+        arr = [(c_double * max(1, n))(*[t[i] for t in terms]) for i in range(3)]
+        _check(lib.ga_set_forcing(self.ctx, _ptr(G) if G is not None else None, n, arr[0], arr[1], arr[2],
+                                  float(t0), self._s()), self.ctx)
 
     def advance(self, nsteps):
         _check(lib.ga_advance(self.ctx, int(nsteps), self._s()), self.ctx)

@@ -1,0 +1,91 @@
+"""GPU parity of the forcing term (eq:ho1 P:398-404, reading: block j takes
+F^{(3j-3)} at t_n + alpha_fj tau, the initial chain F^{(m-2)}(t0)): F(x, t) = G(x) h(t) with a
+sinusoidal h, set through ga_set_forcing, against the oracle (whose reading is pinned by
+test_oracle_integrator.py::test_forced_scalar_ode_order_2k).  Plus a manufactured forced
+solution u = sin(pi x) sin(pi y) h(t) on the GPU alone: order-2k self-convergence and a small
+error against the closed form."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import assembly, integrator
+
+from _helpers import Case, mnorm_rel
+
+pytestmark = pytest.mark.gpu
+TERMS = [(1.0, 30.0, 0.1), (0.3, 55.0, -0.7)]
+
+
+@pytest.mark.parametrize("cfg,op_mode", [
+    (synth.config("c2", n=10, k=2, rho=0.5), 0),
+    (synth.config("c2", n=10, k=1, rho=0.0), 0),
+    (synth.config("c3", p=2, n=5, k=3, rho=1.0), 0),
+    (synth.config("c3", p=3, n=4, k=2, rho=0.5), 2),
+    (synth.config("c3", p=3, n=4, k=2, rho=0.5), 3),
+    (synth.config("c4", p=2, n=3), 0),
+    (synth.config("c5", p=2, n=4), 0),
+], ids=["2d_k2", "2d_k1", "3d_k3_rho1", "3d_matrix_free", "3d_half", "elastic", "lshape"])
+def test_forcing_parity(cfg, op_mode):
+    c = Case(cfg, op_mode=op_mode)
+    d = c.disc
+    u0 = c.u0()
+    v0 = 0.3 * u0
+    G = d.M @ np.cos(np.arange(d.M.shape[0]) * 0.37)  # any load vector; smooth-ish
+    t0, nsteps = 0.2, 25
+    c.ctx.set_forcing(c.to_lib(G), TERMS, t0)
+    c.ctx.set_state(c.to_lib(u0), c.to_lib(v0))
+    c.ctx.advance(nsteps)
+    st = c.ctx.stats()
+    assert st.status == 0 and st.steps == nsteps
+    got = [c.from_lib(t) for t in c.ctx.get_state()]
+    it = integrator.Integrator(d.M, d.K, cfg["k"], cfg["rho"], c.dt, forcing=integrator.Forcing(G, TERMS), t0=t0)
+    ref = it.run(u0, v0, nsteps)
+    errs = [mnorm_rel(d.M, x, y) for x, y in zip(got, ref[:3])]
+    assert max(errs) < 1e-10, errs
+    # removing the forcing restores the homogeneous step
+    c.ctx.set_forcing(None)
+    c.ctx.set_state(c.to_lib(u0), c.to_lib(v0))
+    c.ctx.advance(5)
+    ref0 = integrator.Integrator(d.M, d.K, cfg["k"], cfg["rho"], c.dt).run(u0, v0, 5)
+    assert mnorm_rel(d.M, c.from_lib(c.ctx.get_state()[0]), ref0[0]) < 1e-10
+
+
+def test_forced_manufactured_solution_order():
+    # u = sin(pi x) sin(pi y) h(t), h = cos(3t) + 0.5 cos(5t + 0.3): u_tt - Laplace u =
+    # sin sin (h'' + 2 pi^2 h) -> F = G h_F with G_i = int sin sin B_i, h_F terms a (2 pi^2 - w^2)
+    import torch
+
+    from paper_2102_11536_b200 import Context, make_desc
+    p, n, k, rho, T = 3, 12, 2, 0.5, 0.3
+    ctrl = synth.control_net(2, p, n)
+    d = assembly.Discretization([((0, 0), ctrl)], p, n, 2)
+    Q = assembly.PatchQuad(ctrl, p, n, 2)
+    free = assembly.interior_mask(n + p, 2)
+    Bf = Q.B[:, free]
+    xq = Q.B @ ctrl
+    W = Q.w * Q.detJ
+    g = np.sin(np.pi * xq[:, 0]) * np.sin(np.pi * xq[:, 1])
+    G = Bf.T @ (W * g)
+    hterms = [(1.0, 3.0, 0.0), (0.5, 5.0, 0.3)]
+    fterms = [(a * (2 * np.pi ** 2 - w * w), w, ph) for a, w, ph in hterms]
+    h = lambda t, m=0: sum(a * w ** m * math.cos(w * t + ph + m * math.pi / 2) for a, w, ph in hterms)
+    solve = integrator.DirectMassSolver(d.M)
+    Pg = solve(G)  # L2 projection of sin sin
+    sols = {}
+    for N in (60, 120, 240):
+        desc = make_desc([((0, 0), ctrl)], p, n, 2, k=k, rho=rho, dt=T / N)
+        ctx = Context(desc)
+        ctx.set_forcing(torch.tensor(G, device="cuda"), fterms, 0.0)
+        ctx.set_state(torch.tensor(Pg * h(0.0), device="cuda"), torch.tensor(Pg * h(0.0, 1), device="cuda"))
+        ctx.advance(N)
+        assert ctx.stats().status == 0
+        sols[N] = ctx.get_state()[0].cpu().numpy()
+    M = d.M
+    rel = lambda x, y: math.sqrt((x - y) @ (M @ (x - y)) / (y @ (M @ y)))
+    d1, d2 = rel(sols[60], sols[120]), rel(sols[120], sols[240])
+    assert math.log2(d1 / d2) > 2 * k - 0.4, (d1, d2)
+    ex = g * h(T)
+    e = Bf @ sols[240] - ex
+    assert math.sqrt((W * e * e).sum() / (W * ex * ex).sum()) < 1e-4
