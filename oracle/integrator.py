@@ -21,7 +21,12 @@ Initial chain (P:119-121, P:155-162 generalised, reading R3):
 Forcing (eq:ho1 P:398-404): block j's right-hand side is
 F^{(3j-3)}(t_n + alpha_fj tau) - K s_j, and the initial chain is
 c_m = M^{-1}(F^{(m-2)}(t_0) - K c_{m-2}) (the ODE differentiated m-2 times at t_0).
-Here F(t) = G h(t) with h a sum of sinusoids, whose derivatives are closed form."""
+Here F(t) = G h(t) with h a sum of sinusoids, whose derivatives are closed form.
+
+Damping C (eq:ho1's C L^{3j-4}(A_n) term, reading R16 = SURVEY G8 resolved like R1): block j
+subtracts C w_j with w_j = T_{3j-2}(c) (j < k, the Taylor predictor of its velocity-level
+entry) and w_k = c_{3k-2}; the initial chain c_m = M^{-1}(F^{(m-2)} - K c_{m-2} - C c_{m-1}).
+The literal old value c_{3j-2} for j < k is first order (test_damped_scalar_ode_order_2k)."""
 from __future__ import annotations
 
 import math
@@ -74,18 +79,20 @@ class Forcing:
         return self.h(m, t) * self.G
 
 
-def initial_chain(u0, v0, k: int, solve, Kop, F=None, t0: float = 0.0):
-    """c_0 = U_0, c_1 = V_0, c_m = M^{-1}(F^{(m-2)}(t_0) - K c_{m-2}) for m = 2..3k-1."""
+def initial_chain(u0, v0, k: int, solve, Kop, F=None, t0: float = 0.0, Cop=None):
+    """c_0 = U_0, c_1 = V_0, c_m = M^{-1}(F^{(m-2)}(t_0) - K c_{m-2} - C c_{m-1}), m = 2..3k-1."""
     c = [np.array(u0, dtype=np.float64), np.array(v0, dtype=np.float64)]
     for m in range(2, 3 * k):
         rhs = -(Kop @ c[m - 2])
+        if Cop is not None:
+            rhs = rhs - Cop @ c[m - 1]
         if F is not None:
             rhs = rhs + F(m - 2, t0)
         c.append(solve(rhs))
     return c
 
 
-def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop, F=None, t: float = 0.0, alpha_f=None):
+def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop, F=None, t: float = 0.0, alpha_f=None, Cop=None):
     """One explicit step of the order-2k scheme from time t; returns the new chain."""
     new = [None] * (3 * k)
     for j in range(1, k + 1):
@@ -93,6 +100,8 @@ def step(c, k: int, tau: float, alpha, beta, gamma, solve, Kop, F=None, t: float
         Td, Tv, Ta = taylor(c, d, tau), taylor(c, v, tau), taylor(c, a, tau)
         s = Td if j < k else c[d]
         rhs = -(Kop @ s)
+        if Cop is not None:  # C w_j, w_j = T_vel(c) for j < k, c_vel for j = k (reading R16)
+            rhs = rhs - Cop @ (Tv if j < k else c[v])
         if F is not None:  # F^{(3j-3)} at t_n + alpha_fj tau (eq:ho1)
             rhs = rhs + F(3 * j - 3, t + alpha_f[j - 1] * tau)
         y = solve(rhs)
@@ -107,20 +116,21 @@ class Integrator:
     """Convenience driver: M, K (free-DoF sparse matrices), k, rho, dt."""
 
     def __init__(self, M, K, k: int, rho: float, dt: float, param_set: int = 0, solver=None, forcing=None,
-                 t0: float = 0.0):
+                 t0: float = 0.0, C=None):
         self.M, self.K = sp.csr_matrix(M), sp.csr_matrix(K)
         self.k, self.dt = k, dt
         self.alpha, self.beta, self.gamma, self.alpha_f = scheme_params(k, rho, param_set)
         self.solve = solver if solver is not None else DirectMassSolver(self.M)
         self.F, self.t0, self.n = forcing, t0, 0
+        self.C = None if C is None else sp.csr_matrix(C)
 
     def init(self, u0, v0):
         self.n = 0
-        return initial_chain(u0, v0, self.k, self.solve, self.K, self.F, self.t0)
+        return initial_chain(u0, v0, self.k, self.solve, self.K, self.F, self.t0, self.C)
 
     def step(self, c):
         out = step(c, self.k, self.dt, self.alpha, self.beta, self.gamma, self.solve, self.K, self.F,
-                   self.t0 + self.n * self.dt, self.alpha_f)
+                   self.t0 + self.n * self.dt, self.alpha_f, self.C)
         self.n += 1
         return out
 

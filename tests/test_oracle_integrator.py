@@ -218,3 +218,26 @@ def test_forced_scalar_ode_order_2k(k):
     ou, ov = _orders(errs_u), _orders(errs_v)
     assert ou[-1] > 2 * k - 0.35, (ou, errs_u)
     assert ov[-1] > 2 * k - 0.35, (ov, errs_v)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_damped_scalar_ode_order_2k(k):
+    # Damping (eq:ho1's C term, reading R16): u'' + 2 zeta w u' + w^2 u = 0, u(0) = 1, v(0) = 0,
+    # exact u = e^{-zeta w t}(cos(wd t) + zeta w / wd sin(wd t)).  C acting on the old
+    # velocity-level entry instead of its Taylor predictor drops the order to 1 for k >= 2.
+    w, zeta, T, rho = 1.0, 0.15, 4.0, 0.5
+    wd = w * math.sqrt(1 - zeta ** 2)
+    ue = lambda t: math.exp(-zeta * w * t) * (math.cos(wd * t) + zeta * w / wd * math.sin(wd * t))
+    errs = []
+    taus = [0.2 / 2 ** i for i in range(5)] if k < 3 else [0.4 / 2 ** i for i in range(4)]
+    for tau in taus:
+        it = integrator.Integrator(np.eye(1), np.array([[w * w]]), k, rho, tau, solver=lambda b: b,
+                                   C=np.array([[2 * zeta * w]]))
+        c = it.init(np.array([1.0]), np.array([0.0]))
+        e = 0.0
+        for n in range(1, int(round(T / tau)) + 1):
+            c = it.step(c)
+            e = max(e, abs(c[0][0] - ue(n * tau)))
+        errs.append(e)
+    o = _orders(errs)
+    assert o[-1] > 2 * k - 0.35, (o, errs)
