@@ -98,6 +98,9 @@ typedef struct {
                         /*    per apply, half the memory; the elastic K stays full);    */
                         /* 0: auto = full stencils if they fit in ~150 GB, else half-   */
                         /*    symmetric, else matrix-free (measured, R14)     */
+  double damp_a0, damp_a1; /* Rayleigh damping C = damp_a0 M + damp_a1 K, >= 0 (SURVEY    */
+                        /* NEXT-2; reading R16: block j subtracts C w_j, w_j the Taylor */
+                        /* predictor of its velocity-level entry for j < k); 0 0: none  */
 } ga_desc;
 
 typedef struct {

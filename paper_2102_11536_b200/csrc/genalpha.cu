@@ -146,6 +146,10 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
   if (!(d->pcg_rtol > 0.0) || d->pcg_maxit < 1) { seterr(ctx, "pcg_rtol > 0 and pcg_maxit >= 1 required"); return GA_ERR_ARG; }
   if (d->param_set != 0 && d->param_set != 1) { seterr(ctx, "param_set must be 0 or 1"); return GA_ERR_ARG; }
   if (d->op_mode < 0 || d->op_mode > 3) { seterr(ctx, "op_mode must be 0, 1, 2 or 3"); return GA_ERR_ARG; }
+  if (!std::isfinite(d->damp_a0) || !std::isfinite(d->damp_a1) || d->damp_a0 < 0.0 || d->damp_a1 < 0.0) {
+    seterr(ctx, "damping coefficients must be finite and >= 0");
+    return GA_ERR_ARG;
+  }
   if (d->op_mode == 2 && d->npatch != 1) { seterr(ctx, "op_mode 2 (matrix-free) supports a single patch"); return GA_ERR_ARG; }
   double a[KMAX], b[KMAX], g[KMAX], f[KMAX], th;
   int rc = scheme_params(d->k, d->rho_b, d->rho_s, d->param_set, a, b, g, f, &th);
@@ -487,6 +491,7 @@ StageArgs stage_args(ga_ctx* c) {
   }
   a.tau = c->d.dt;
   a.unstable2 = c->d.unstable_factor > 0 ? c->d.unstable_factor * c->d.unstable_factor : 0.0;
+  a.damp_a0 = c->d.damp_a0; a.damp_a1 = c->d.damp_a1;
   a.st = c->st; a.partial = c->partial; a.counter = c->counter;
   return a;
 }
@@ -1111,11 +1116,13 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
   if (d_v0) launch_api_to_grid(ctx->g, nvec, ctx->nfree, ctx->map, d_v0, ctx->chain + vstride, 1, 0, ctx->st, s);
   CK(cudaGetLastError());
   // c_m = M^{-1}(-K c_{m-2}), m = 2..3k-1, two at a time when k >= 2
-  const int batch = std::min(2, k);
+  // damping couples c_m to c_{m-1}: the chain entries are then solved one at a time
+  const bool damped = ctx->d.damp_a0 != 0.0 || ctx->d.damp_a1 != 0.0;
+  const int batch = damped ? 1 : std::min(2, k);
   for (int m0 = 2; m0 <= 3 * k - 1; m0 += batch) {
-    int src[KMAX] = {-1, -1, -1, -1}, dst[KMAX] = {-1, -1, -1, -1};
+    int src[KMAX] = {-1, -1, -1, -1}, dst[KMAX] = {-1, -1, -1, -1}, src2[KMAX] = {-1, -1, -1, -1};
     for (int j = 0; j < batch; ++j)
-      if (m0 + j <= 3 * k - 1) { src[j] = m0 + j - 2; dst[j] = m0 + j; }
+      if (m0 + j <= 3 * k - 1) { src[j] = m0 + j - 2; dst[j] = m0 + j; if (damped) src2[j] = m0 + j - 1; }
     if (ctx->forcing) {  // c_m = M^{-1}(F^{(m-2)}(t0) - K c_{m-2}) (eq:ho1 differentiated)
       ForceSlots fs;
       memset(&fs, 0, sizeof(fs));
@@ -1123,10 +1130,11 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
         if (dst[j] >= 0) { fs.active[j] = 1; fs.order[j] = dst[j] - 2; fs.toff[j] = 0.0; }
       CK(cudaMemcpyAsync(ctx->fslots, &fs, sizeof(fs), cudaMemcpyHostToDevice, s));
     }
-    launch_pack(ctx->g, nvec, k, ctx->chain, src, ctx->pred, ctx->st, s);
+    // c_m = M^{-1}(F^{(m-2)} - K (c_{m-2} + a1 c_{m-1})) - a0 c_{m-1}  (Rayleigh C = a0 M + a1 K)
+    launch_pack(ctx->g, nvec, k, ctx->chain, src, ctx->pred, ctx->st, s, src2, ctx->d.damp_a1);
     rc = run_kind(ctx, GK_SOLVEK, s);
     if (rc != GA_OK) return rc;
-    launch_unpack(ctx->g, nvec, k, ctx->x, dst, ctx->chain, ctx->st, s);
+    launch_unpack(ctx->g, nvec, k, ctx->x, dst, ctx->chain, ctx->st, s, src2, ctx->d.damp_a0);
     CK(cudaGetLastError());
   }
   return set_predictors_and_norm(ctx, s);

@@ -1002,7 +1002,9 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
           for (int j = 0; j < K; ++j) {
             const int d = 3 * j, v = 3 * j + 1, ac = 3 * j + 2;
             const double Td = taylor_k<K>(cc, d, f), Tv = taylor_k<K>(cc, v, f), Ta = taylor_k<K>(cc, ac, f);
-            const double P = (y[j] - Ta) / a.alpha[j];
+            // Rayleigh damping (reading R16): y_j - a0 w_j, w_j = T_vel (j < k), c_vel (j = k)
+            const double wj = (j < K - 1) ? Tv : cc[v];
+            const double P = (fma(-a.damp_a0, wj, y[j]) - Ta) / a.alpha[j];
             nw[d] = fma(a.beta[j] * a.tau * a.tau, P, Td);
             nw[v] = fma(a.gamma[j] * a.tau, P, Tv);
             nw[ac] = Ta + P;
@@ -1015,7 +1017,12 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
         }
         // predictors of the next step: s_j = T_disp(c) (j < k), s_k = c_{3k-3}
 #pragma unroll
-        for (int j = 0; j < K; ++j) a.pred[off * K + j] = (j < K - 1) ? taylor_k<K>(nw, 3 * j, f) : nw[3 * j];
+        for (int j = 0; j < K; ++j) {
+          // K acts on s_j + a1 w_j (Rayleigh damping folded into the -K s SpMV; a1 = 0: s_j exactly)
+          const double sj = (j < K - 1) ? taylor_k<K>(nw, 3 * j, f) : nw[3 * j];
+          const double wj = (j < K - 1) ? taylor_k<K>(nw, 3 * j + 1, f) : nw[3 * j + 1];
+          a.pred[off * K + j] = fma(a.damp_a1, wj, sj);
+        }
         u2[0] = fma(nw[0], nw[0], u2[0]);
       }
     }
@@ -1088,7 +1095,9 @@ void launch_predict(const StageArgs& a, cudaStream_t s) { stage_go<false>(a, s);
 // ---------------------------------------------------------------------------
 struct Idx4 { int v[KMAX]; };
 
-__global__ void k_pack(GridDesc g, int nvec, int kk, const double* chain, Idx4 src, double* mv, DevStatus* st) {
+// mv slot j = chain[src_j] + a1 chain[src2_j]  (src2 < 0: no damping term)
+__global__ void k_pack(GridDesc g, int nvec, int kk, const double* chain, Idx4 src, Idx4 src2, double a1, double* mv,
+                       DevStatus* st) {
   count_launch(st);
   const long long tot = (long long)nvec * g.npts * kk;
   const long long e = (long long)gtid();
@@ -1098,10 +1107,13 @@ __global__ void k_pack(GridDesc g, int nvec, int kk, const double* chain, Idx4 s
   const long long i = ci % g.npts;
   const int c = (int)(ci / g.npts);
   const long long vstride = (long long)nvec * g.padded;
-  const double v = src.v[j] >= 0 ? chain[src.v[j] * vstride + (long long)c * g.padded + g.guard + i] : 0.0;
+  double v = src.v[j] >= 0 ? chain[src.v[j] * vstride + (long long)c * g.padded + g.guard + i] : 0.0;
+  if (src2.v[j] >= 0) v = fma(a1, chain[src2.v[j] * vstride + (long long)c * g.padded + g.guard + i], v);
   mv[((long long)c * g.padded + g.guard + i) * kk + j] = v;
 }
-__global__ void k_unpack(GridDesc g, int nvec, int kk, const double* mv, Idx4 dst, double* chain, DevStatus* st) {
+// chain[dst_j] = mv slot j - a0 chain[src2_j]  (src2 < 0: no damping term)
+__global__ void k_unpack(GridDesc g, int nvec, int kk, const double* mv, Idx4 dst, Idx4 src2, double a0, double* chain,
+                         DevStatus* st) {
   count_launch(st);
   const long long tot = (long long)nvec * g.npts * kk;
   const long long e = (long long)gtid();
@@ -1112,21 +1124,23 @@ __global__ void k_unpack(GridDesc g, int nvec, int kk, const double* mv, Idx4 ds
   const long long i = ci % g.npts;
   const int c = (int)(ci / g.npts);
   const long long vstride = (long long)nvec * g.padded;
-  chain[dst.v[j] * vstride + (long long)c * g.padded + g.guard + i] = mv[((long long)c * g.padded + g.guard + i) * kk + j];
+  double v = mv[((long long)c * g.padded + g.guard + i) * kk + j];
+  if (src2.v[j] >= 0) v = fma(-a0, chain[src2.v[j] * vstride + (long long)c * g.padded + g.guard + i], v);
+  chain[dst.v[j] * vstride + (long long)c * g.padded + g.guard + i] = v;
 }
 void launch_pack(const GridDesc& g, int nvec, int kk, const double* chain, const int* src, double* mv,
-                 DevStatus* st, cudaStream_t s) {
-  Idx4 ix;
-  for (int j = 0; j < KMAX; ++j) ix.v[j] = j < kk ? src[j] : -1;
+                 DevStatus* st, cudaStream_t s, const int* src2, double a1) {
+  Idx4 ix, ix2;
+  for (int j = 0; j < KMAX; ++j) { ix.v[j] = j < kk ? src[j] : -1; ix2.v[j] = (src2 && j < kk) ? src2[j] : -1; }
   const long long tot = (long long)nvec * g.npts * kk;
-  k_pack<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, chain, ix, mv, st);
+  k_pack<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, chain, ix, ix2, a1, mv, st);
 }
 void launch_unpack(const GridDesc& g, int nvec, int kk, const double* mv, const int* dst, double* chain,
-                   DevStatus* st, cudaStream_t s) {
-  Idx4 ix;
-  for (int j = 0; j < KMAX; ++j) ix.v[j] = j < kk ? dst[j] : -1;
+                   DevStatus* st, cudaStream_t s, const int* src2, double a0) {
+  Idx4 ix, ix2;
+  for (int j = 0; j < KMAX; ++j) { ix.v[j] = j < kk ? dst[j] : -1; ix2.v[j] = (src2 && j < kk) ? src2[j] : -1; }
   const long long tot = (long long)nvec * g.npts * kk;
-  k_unpack<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, mv, ix, chain, st);
+  k_unpack<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(g, nvec, kk, mv, ix, ix2, a0, chain, st);
 }
 
 // api[c*nfree + f] <-> grid[((c*padded + guard + map[f]) * kk + slot)]

@@ -115,6 +115,7 @@ struct StageArgs {
   double f[3 * KMAX];   // tau^i / i!
   double tau;
   double unstable2;     // threshold on ||U||^2 / ||U0||^2 (0: off)
+  double damp_a0, damp_a1;  // Rayleigh damping C = a0 M + a1 K (reading R16)
   DevStatus* st;
   double* partial;
   unsigned int* counter;
@@ -147,10 +148,11 @@ void launch_add_forcing(const ForceArgs& a, cudaStream_t s);
 void launch_predict(const StageArgs& a, cudaStream_t s);
 
 // chain <-> MV slot packing for the initial chain (src/dst < 0: zero / skip).
+// with damping: pack slot = chain[src] + a1 chain[src2], unpack chain[dst] = slot - a0 chain[src2]
 void launch_pack(const GridDesc& g, int nvec, int kk, const double* chain, const int* src, double* mv,
-                 DevStatus* st, cudaStream_t s);
+                 DevStatus* st, cudaStream_t s, const int* src2 = nullptr, double a1 = 0.0);
 void launch_unpack(const GridDesc& g, int nvec, int kk, const double* mv, const int* dst, double* chain,
-                   DevStatus* st, cudaStream_t s);
+                   DevStatus* st, cudaStream_t s, const int* src2 = nullptr, double a0 = 0.0);
 
 // free-DoF (API) vector <-> grid vector (stride kk, slot j) with optional map
 void launch_api_to_grid(const GridDesc& g, int nvec, long long nfree, const long long* map, const double* api,

@@ -38,7 +38,8 @@ class ga_desc(ctypes.Structure):
                 ("lame_mu", c_double), ("density", c_double), ("k", c_int), ("rho_b", c_double),
                 ("rho_s", c_double), ("param_set", c_int), ("dt", c_double), ("pcg_rtol", c_double),
                 ("pcg_maxit", c_int), ("pcg_refine", c_int), ("pcg_refine_rtol", c_double),
-                ("unstable_factor", c_double), ("op_mode", c_int)]
+                ("unstable_factor", c_double), ("op_mode", c_int), ("damp_a0", c_double),
+                ("damp_a1", c_double)]
 
 
 class ga_stats(ctypes.Structure):
@@ -112,7 +113,7 @@ def ga_params(k, rho_b, rho_s=None, param_set=0):
 
 def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3, param_set=0,
               omega=1.0, lam=1.0, mu=1.0, density=1.0, pcg_rtol=1e-13, pcg_maxit=500,
-              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6, op_mode=0):
+              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6, op_mode=0, damp_a0=0.0, damp_a1=0.0):
     """ga_desc from [(cell, ctrl ndarray (m^dim, dim))].  Keeps the ctrl arrays
     alive on the returned object (`_keep`)."""
     arr = (ga_patch * len(patches))()
@@ -130,7 +131,7 @@ def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3,
                 # refinement restart (R8): needed where kappa(M) ~1e7-1e8 (3D p >= 5)
                 pcg_refine=(1 if p >= 5 else 0) if pcg_refine is None else pcg_refine,
                 pcg_refine_rtol=(1e-3 if p >= 5 else 0.0) if pcg_refine_rtol is None else pcg_refine_rtol,
-                unstable_factor=unstable_factor, op_mode=op_mode)
+                unstable_factor=unstable_factor, op_mode=op_mode, damp_a0=damp_a0, damp_a1=damp_a1)
     d._keep = (arr, keep)
     return d
 

@@ -89,3 +89,40 @@ def test_forced_manufactured_solution_order():
     ex = g * h(T)
     e = Bf @ sols[240] - ex
     assert math.sqrt((W * e * e).sum() / (W * ex * ex).sum()) < 1e-4
+
+
+@pytest.mark.parametrize("cfg,op_mode,forced", [
+    (synth.config("c2", n=10, k=2, rho=0.5), 0, False),
+    (synth.config("c2", n=10, k=3, rho=0.0), 0, True),
+    (synth.config("c2", n=10, k=1, rho=0.5), 0, True),
+    (synth.config("c3", p=2, n=5, k=2, rho=0.5), 0, True),
+    (synth.config("c3", p=3, n=4, k=2, rho=0.5), 3, False),
+    (synth.config("c3", p=3, n=4, k=2, rho=0.5), 2, True),
+    (synth.config("c4", p=2, n=3), 0, False),
+    (synth.config("c5", p=2, n=4), 0, True),
+], ids=["2d_k2", "2d_k3_forced", "2d_k1_forced", "3d_forced", "3d_half", "3d_matrix_free_forced", "elastic",
+        "lshape_forced"])
+def test_rayleigh_damping_parity(cfg, op_mode, forced):
+    # C = a0 M + a1 K (reading R16, pinned by test_oracle_integrator.py::test_damped_scalar_ode_order_2k)
+    base = Case(cfg, op_mode=op_mode)
+    lam = base.lam_max
+    a0, a1 = 0.8 * math.sqrt(lam) * 0.05, 0.3 / math.sqrt(lam)
+    c = Case(cfg, op_mode=op_mode, dt=base.dt, damp_a0=a0, damp_a1=a1)
+    d = c.disc
+    u0 = c.u0()
+    v0 = -0.2 * u0
+    F = None
+    if forced:
+        G = d.M @ np.cos(np.arange(d.M.shape[0]) * 0.37)
+        c.ctx.set_forcing(c.to_lib(G), TERMS, 0.1)
+        F = integrator.Forcing(G, TERMS)
+    c.ctx.set_state(c.to_lib(u0), c.to_lib(v0))
+    nsteps = 25
+    c.ctx.advance(nsteps)
+    st = c.ctx.stats()
+    assert st.status == 0 and st.steps == nsteps
+    got = [c.from_lib(t) for t in c.ctx.get_state()]
+    it = integrator.Integrator(d.M, d.K, cfg["k"], cfg["rho"], c.dt, forcing=F, t0=0.1, C=a0 * d.M + a1 * d.K)
+    ref = it.run(u0, v0, nsteps)
+    errs = [mnorm_rel(d.M, x, y) for x, y in zip(got, ref[:3])]
+    assert max(errs) < 1e-10, errs
