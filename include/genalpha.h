@@ -185,9 +185,10 @@ ga_status ga_apply(ga_ctx* ctx, int which, const double* d_x, double* d_y, void*
  * SYNCHRONIZES stream. */
 ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters, void* stream);
 
-/* lambda_max(M^{-1} K) by `iters` power iterations (each one K apply + one PCG
- * solve), for the CFL time step dt = c sqrt(theta_max / lambda_max).
- * SYNCHRONIZES stream. */
+/* lambda_max(M^{-1} K) by `iters` (<= 512) Lanczos steps in the M inner product (each one K
+ * apply, one PCG mass solve and one M apply; no reorthogonalisation: the extremal Ritz value
+ * converges first), for the CFL time step dt = c sqrt(theta_max / lambda_max).  The time-
+ * stepping state is left unchanged.  SYNCHRONIZES stream. */
 ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream);
 
 /* host_map[f] = patch * (n+p)^dim + local control-point index (co-lex) of

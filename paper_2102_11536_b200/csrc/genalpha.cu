@@ -84,6 +84,7 @@ struct ga_ctx {
   double* forceG = nullptr;
   ForceSlots* fslots = nullptr;
   bool forcing = false;
+  double *lzv = nullptr, *lzab = nullptr;  // Lanczos vectors and alpha/beta (ga_lambda_max)
   int fnterms = 0;
   double famp[FMAXTERMS], fomega[FMAXTERMS], fphase[FMAXTERMS], ft0 = 0.0;
   long long mfws = 0;    // Gauss points (n(p+1))^dim
@@ -110,7 +111,8 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t off_coefM, off_coefK, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
-      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots;
+      off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots,
+      off_lz, off_lzab;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
 };
@@ -304,6 +306,8 @@ int op_auto(const ga_desc* d) {
   return d->npatch == 1 ? 2 : 3;
 }
 
+constexpr int LZMAX = 512;  // Lanczos steps of ga_lambda_max
+
 size_t sweep_bytes(int n, int p) {
   // dinv + coef + H + A (L <= 6 levels, C <= 64 chunks)
   return align256(sizeof(double) * ((size_t)n * (1 + 2 * p) + (size_t)6 * 64 * p * p));
@@ -356,6 +360,8 @@ Layout make_layout(const Shape& sh) {
   L.off_dscal = take(sizeof(double) * 16);
   L.off_forceG = take(sizeof(double) * sh.nvec * sh.g.padded);
   L.off_fslots = take(sizeof(ForceSlots));
+  L.off_lz = take(sizeof(double) * 2 * sh.nvec * sh.g.padded * sh.k);  // Lanczos v_{j-1}, v_j (MV layout)
+  L.off_lzab = take(sizeof(double) * 2 * (LZMAX + 2));
   for (size_t r = 0; r < sh.prec.size(); ++r) {
     const PrecPatch& pp = sh.prec[r];
     long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
@@ -945,6 +951,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->dscal = (double*)(ws + L.off_dscal);
   ctx->forceG = (double*)(ws + L.off_forceG);
   ctx->fslots = (ForceSlots*)(ws + L.off_fslots);
+  ctx->lzv = (double*)(ws + L.off_lz);
+  ctx->lzab = (double*)(ws + L.off_lzab);
 #define CKD(call)                           \
   do {                                      \
     cudaError_t e_ = (call);                \
@@ -1066,6 +1074,33 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   *out = ctx;
   return GA_OK;
 }
+
+// Lanczos for M^{-1} K in the M inner product (slot 0 of MV-layout vectors, stride kk):
+// w = A v_j - alpha_j v_j - beta_{j-1} v_{j-1} with A v_j = -x (x = M^{-1}(-K v_j)),
+// alpha_j = v_j.K v_j = -(v_j . b) (b = -K v_j); written into vn (= v_{j-1}'s buffer)
+__global__ void k_lz_update(GridDesc g, int nvec, int kk, const double* x, const double* v, double* vn,
+                            const double* dal, const double* dbe, const unsigned char* mask) {
+  const long long tot = (long long)nvec * g.npts;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const long long c = e / g.npts, i = e - c * g.npts;
+  const long long o = (c * g.padded + g.guard + i) * kk;
+  const double al = -dal[0], be = dbe[0];
+  double w = -x[o] - al * v[o] - be * vn[o];
+  if (mask && !mask[i]) w = 0.0;
+  vn[o] = w;
+}
+// v *= 1 / sqrt(d[0]) and record beta = sqrt(d[0]) in rec (device)
+__global__ void k_lz_norm(GridDesc g, int nvec, int kk, double* v, const double* d, double* rec) {
+  const double b = sqrt(fmax(d[0], 0.0));
+  if (blockIdx.x == 0 && threadIdx.x == 0) rec[0] = b;
+  const long long tot = (long long)nvec * g.npts;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot || b == 0.0) return;
+  const long long c = e / g.npts, i = e - c * g.npts;
+  v[(c * g.padded + g.guard + i) * kk] *= 1.0 / b;
+}
+__global__ void k_lz_copy_alpha(const double* src, double* dst) { dst[0] = -src[0]; }
 
 __global__ void k_reset_status(DevStatus* st, PcgState* pc) {
   memset(st, 0, sizeof(DevStatus));
@@ -1334,45 +1369,94 @@ ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters,
 }
 
 ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
+  // lambda_max(M^{-1} K) by Lanczos in the M inner product: each step
+  // one K apply + one PCG mass solve (the K-solve graph) + one M apply; the alpha/beta stay on
+  // the device, the largest eigenvalue of the tridiagonal matrix is found on the host
   ga_status rc = check_ctx(ctx);
   if (rc != GA_OK) return rc;
   if (iters < 1 || !lam) { seterr(ctx, "iters >= 1 and lam required"); return GA_ERR_ARG; }
+  iters = std::min(iters, LZMAX);
   cudaStream_t s = (cudaStream_t)stream;
   const GridDesc& g = ctx->g;
   const int nvec = ctx->nvec, k = ctx->k;
   const size_t mvbytes = sizeof(double) * nvec * g.padded * k;
+  const long long tot = (long long)nvec * g.npts;
+  const unsigned int nb = (unsigned int)((tot + 255) / 256);
   // the predictor MV is state: keep a host copy and restore it at the end
   std::vector<double> hsave(mvbytes / sizeof(double));
   CK(cudaMemcpyAsync(hsave.data(), ctx->pred, mvbytes, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  CK(cudaMemsetAsync(ctx->pred, 0, mvbytes, s));
-  const long long tot = (long long)nvec * g.npts;
-  k_altsign<<<(unsigned int)((tot + 255) / 256), 256, 0, s>>>(g, nvec, k, ctx->pred, ctx->mask);
-  double* dn = ctx->dscal;
-  for (int it = 0; it < iters; ++it) {
-    // normalise v (slot 0 of pred)
-    launch_dot(g, nvec, k, ctx->pred, ctx->pred, dn, ctx->partial, ctx->counter, s);
-    launch_scale(g, nvec, k, ctx->pred, dn, 1, s);
-    rc = run_kind(ctx, GK_SOLVEK, s);  // x = M^{-1}(-K v)
-    if (rc != GA_OK) return rc;
-    // v <- x (slot 0)
-    CK(cudaMemcpyAsync(ctx->pred, ctx->x, mvbytes, cudaMemcpyDeviceToDevice, s));
+  if (ctx->forcing) {  // the K-solve graph would add F: switch the slots off meanwhile
+    ForceSlots fs;
+    memset(&fs, 0, sizeof(fs));
+    CK(cudaMemcpyAsync(ctx->fslots, &fs, sizeof(fs), cudaMemcpyHostToDevice, s));
   }
-  // Rayleigh quotient (v.Kv)/(v.Mv)
-  launch_dot(g, nvec, k, ctx->pred, ctx->pred, dn, ctx->partial, ctx->counter, s);
-  launch_scale(g, nvec, k, ctx->pred, dn, 1, s);
-  launch_spmv(spmv_args(ctx, 1, ctx->pred, ctx->q, SPMV_APPLY), s);
-  launch_dot(g, nvec, k, ctx->pred, ctx->q, dn + 1, ctx->partial, ctx->counter, s);
-  launch_spmv(spmv_args(ctx, 0, ctx->pred, ctx->q, SPMV_APPLY), s);
-  launch_dot(g, nvec, k, ctx->pred, ctx->q, dn + 2, ctx->partial, ctx->counter, s);
-  double hv[3];
-  CK(cudaMemcpyAsync(hv, dn, sizeof(hv), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  double* vp = ctx->lzv;                                   // v_{j-1} (then w)
+  double* vc = ctx->lzv + (size_t)nvec * g.padded * k;     // v_j
+  double* al = ctx->lzab;                                  // alpha_j, j < iters
+  double* be = ctx->lzab + LZMAX + 2;                      // beta_j (be[0] = norm of the start vector)
+  double* dn = ctx->dscal;
+  CK(cudaMemsetAsync(ctx->lzv, 0, 2 * mvbytes, s));
+  CK(cudaMemsetAsync(ctx->lzab, 0, sizeof(double) * 2 * (LZMAX + 2), s));
+  k_altsign<<<nb, 256, 0, s>>>(g, nvec, k, vc, ctx->mask);
+  // v_1 = v / ||v||_M
+  launch_spmv(spmv_args(ctx, 0, vc, ctx->q, SPMV_APPLY), s);
+  launch_dot(g, nvec, k, vc, ctx->q, dn, ctx->partial, ctx->counter, s);
+  k_lz_norm<<<nb, 256, 0, s>>>(g, nvec, k, vc, dn, be);
+  int done = iters;
+  for (int j = 0; j < iters; ++j) {
+    CK(cudaMemsetAsync(ctx->pred, 0, mvbytes, s));
+    CK(cudaMemcpy2DAsync(ctx->pred, sizeof(double) * k, vc, sizeof(double) * k, sizeof(double),
+                         (size_t)nvec * g.padded, cudaMemcpyDeviceToDevice, s));
+    rc = run_kind(ctx, GK_SOLVEK, s);  // b = -K v_j, x = M^{-1} b
+    if (rc != GA_OK) return rc;
+    launch_dot(g, nvec, k, vc, ctx->b, dn, ctx->partial, ctx->counter, s);  // -alpha_j
+    k_lz_copy_alpha<<<1, 1, 0, s>>>(dn, al + j);
+    // w = A v_j - alpha_j v_j - beta_{j-1} v_{j-1}, into vp
+    k_lz_update<<<nb, 256, 0, s>>>(g, nvec, k, ctx->x, vc, vp, dn, be + j, ctx->mask);
+    launch_spmv(spmv_args(ctx, 0, vp, ctx->q, SPMV_APPLY), s);
+    launch_dot(g, nvec, k, vp, ctx->q, dn + 1, ctx->partial, ctx->counter, s);
+    k_lz_norm<<<nb, 256, 0, s>>>(g, nvec, k, vp, dn + 1, be + j + 1);
+    std::swap(vp, vc);  // v_{j+1} = w / beta_j becomes current, v_j previous
+    CK(cudaGetLastError());
+  }
+  std::vector<double> ha(done), hb(done + 1);
+  CK(cudaMemcpyAsync(ha.data(), al, sizeof(double) * done, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hb.data(), be, sizeof(double) * (done + 1), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(ctx->pred, hsave.data(), mvbytes, cudaMemcpyHostToDevice, s));
   DevStatus hs;
   CK(cudaMemcpyAsync(&hs, ctx->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  *lam = hv[1] / hv[2];
+  rc = set_step_slots(ctx, s);
+  if (rc != GA_OK) return rc;
   if (hs.status != 0) return (ga_status)hs.status;
+  // stop at a (numerically) invariant subspace: beta_j ~ 0
+  int m = done;
+  for (int j = 1; j < done; ++j)
+    if (!(hb[j] > 1e-14 * std::fabs(ha[0]))) { m = j; break; }
+  // largest eigenvalue of the symmetric tridiagonal T (diag ha, off-diag hb[1..m-1]) by bisection
+  double lo = 1e300, hi = -1e300;
+  for (int j = 0; j < m; ++j) {
+    const double r = (j > 0 ? std::fabs(hb[j]) : 0.0) + (j + 1 < m ? std::fabs(hb[j + 1]) : 0.0);
+    lo = std::min(lo, ha[j] - r);
+    hi = std::max(hi, ha[j] + r);
+  }
+  auto count_below = [&](double x) {  // Sturm count of eigenvalues < x
+    int c = 0;
+    double d = 1.0;
+    for (int j = 0; j < m; ++j) {
+      const double off = j > 0 ? hb[j] * hb[j] : 0.0;
+      d = (ha[j] - x) - (j > 0 ? off / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0.0) ++c;
+    }
+    return c;
+  };
+  for (int it = 0; it < 200 && hi - lo > 1e-15 * std::max(1.0, std::fabs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (count_below(mid) < m) lo = mid; else hi = mid;
+  }
+  *lam = 0.5 * (lo + hi);
   return GA_OK;
 }
 

@@ -89,3 +89,23 @@ def test_op_mode_validation():
     with pytest.raises(GAError) as ei:
         Context(make_desc(prob["patches"], cfg["p"], cfg["n"], 2, k=2, rho=0.0, dt=1e-4, op_mode=7))
     assert ei.value.code == -1
+
+
+@pytest.mark.parametrize("cfg", [synth.config("c1"), synth.config("c2", n=12), synth.config("c3", p=3, n=4),
+                                 synth.config("c4", p=2, n=3), synth.config("c5", p=2, n=4)],
+                         ids=["c1", "2d_deformed", "3d_p3", "elastic", "lshape"])
+def test_lambda_max_lanczos(cfg):
+    # ga_lambda_max (Lanczos in the M inner product) against the oracle's
+    # generalized eigensolver; the time-stepping state must be left unchanged
+    c = Case(cfg)
+    u0 = c.u0()
+    c.ctx.set_state(c.to_lib(u0))
+    c.ctx.advance(2)
+    before = [t.clone() for t in c.ctx.get_state()]
+    lam = c.ctx.lambda_max(80)
+    assert abs(lam - c.lam_max) <= 1e-8 * c.lam_max, (lam, c.lam_max)
+    after = c.ctx.get_state()
+    for x, y in zip(before, after):
+        assert bool((x == y).all())
+    c.ctx.advance(1)
+    assert c.ctx.stats().status == 0
