@@ -63,6 +63,116 @@ __global__ void __launch_bounds__(32 * G) k_spmv_half(SpmvArgs a) {
   }
 }
 
+// Row-tiled SpMV for several component vectors sharing one scalar stencil (the elastic mass,
+// density * M per component): a CTA of TYR warps owns a 32 (x) x TYR (y) tile of rows at one z;
+// for each z offset o3 it stages the (TYR + 2P) y-lines x (32 + 2P) points x NC components of
+// the input once in shared memory (double-buffered, the next plane prefetched into registers),
+// and warp w computes row y0 + w from it.  The TYR rows share every staged input line: the
+// window traffic per row drops from NC (32 + 2P)/32 lines per offset line to
+// NC (TYR + 2P)(32 + 2P) / (32 TYR W) (about 3x less for P = 4).  Linear addressing: points
+// outside the grid in x or y wrap into neighbouring lines, whose coefficients are zero.
+template <int P, int NC, int KK, int TYR>
+__global__ void __launch_bounds__(32 * TYR) k_spmv_tile(SpmvArgs a, int ntx, int nty) {
+  constexpr int W = 2 * P + 1, TX = 32 + 2 * P, TY = TYR + 2 * P;
+  constexpr int PLANE = TY * TX * NC * KK;
+  constexpr int NT = 32 * TYR;
+  if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.st->launches, 1ull);
+  extern __shared__ double smem_t[];
+  double* buf0 = smem_t;
+  double* buf1 = smem_t + PLANE;
+  const GridDesc g = a.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = blockIdx.x % ntx;
+  const int ty = (blockIdx.x / ntx) % nty;
+  const int z = blockIdx.x / (ntx * nty);
+  const int x0 = tx * 32, y0 = ty * TYR;
+  const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+  const int x = x0 + lane, y = y0 + w;
+  const bool valid = x < g.nx && y < g.ny;
+  const long long i = x + sy * y + sz * z;
+  const long long icl = valid ? i : 0;
+  const long long S = (long long)W * W * W;
+  const double* __restrict__ cslice = a.coef + (icl >> 5) * S * 32 + (icl & 31);
+  // staged point q = (ty', tx', c, j) of plane o3: linear index of (x0 - P + tx', y0 - P + ty', z + o3);
+  // copied asynchronously (cp.async, no registers), the next plane while this one is consumed
+  auto issue_plane = [&](int o3, double* dst) {
+    for (int q = threadIdx.x; q < PLANE; q += NT) {
+      const int j = q % KK, c = (q / KK) % NC, txp = (q / (KK * NC)) % TX, typ = q / (KK * NC * TX);
+      const long long pos = g.guard + (x0 - P + txp) + sy * (y0 - P + typ) + sz * (z + o3);
+      const unsigned int d = (unsigned int)__cvta_generic_to_shared(dst + q);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
+                   "l"(a.x + ((long long)c * g.padded + pos) * KK + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double acc[NC][KK];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) acc[c][j] = 0.0;
+  issue_plane(-P, buf0);
+  double cf[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) cf[u] = __ldg(cslice + (long long)u * 32);  // line (o3, o2) = (-P, -P)
+  for (int o3i = 0; o3i < W; ++o3i) {
+    double* cur = (o3i & 1) ? buf1 : buf0;
+    double* nxt = (o3i & 1) ? buf0 : buf1;
+    if (o3i + 1 < W) {
+      issue_plane(o3i + 1 - P, nxt);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this plane's copies are done
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int o2i = 0; o2i < W; ++o2i) {
+      double cc[W];
+#pragma unroll
+      for (int u = 0; u < W; ++u) cc[u] = cf[u];
+      const int line = o3i * W + o2i;
+      if (line + 1 < W * W) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) cf[u] = __ldg(cslice + ((long long)(line + 1) * W + u) * 32);
+      }
+      const double* row = cur + ((w + o2i) * TX + lane) * NC * KK;  // staged y-line y + o2, x from x - P
+#pragma unroll
+      for (int u = 0; u < W; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int j = 0; j < KK; ++j) acc[c][j] = fma(cc[u], row[(u * NC + c) * KK + j], acc[c][j]);
+    }
+    __syncthreads();  // every warp is done with cur before it is refilled
+  }
+  double dots[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) dots[j] = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+      double pv[KK];
+      if (a.mode == SPMV_PQ) load_row<KK>(a.x + base, pv);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        double v = acc[c][j];
+        if (a.mode == SPMV_NEGB) v = -v;
+        else if (a.mode == SPMV_TRUERES) { v = a.b[base + j] - v; dots[j] = fma(v, v, dots[j]); }
+        else if (a.mode == SPMV_PQ) dots[j] = fma(pv[j], v, dots[j]);
+        a.y[base + j] = v;
+      }
+    }
+  }
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) {
+    block_sum<KK>(dots);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < KK; ++j) a.partial[(size_t)blockIdx.x * KK + j] = dots[j];
+    }
+  }
+}
+
 // Fixed-order sum of the SpMV block partials and the PCG scalar step:
 // SPMV_PQ: alpha_j = r.z / p.q (F2); SPMV_TRUERES: restart of the refinement phase.
 template <int KK>
@@ -123,6 +233,25 @@ static void launch_sm(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
 }
 
 template <int P, int NC, int KK>
+static bool launch_tile(const SpmvArgs& a, cudaStream_t s) {
+  constexpr int TYR = 4, TX = 32 + 2 * P, TY = TYR + 2 * P;
+  constexpr size_t bytes = sizeof(double) * 2 * TY * TX * NC * KK;
+  if (bytes > 200 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_spmv_tile<P, NC, KK, TYR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+        cudaSuccess)
+      return false;
+    attr = true;
+  }
+  const int ntx = (a.g.nx + 31) / 32, nty = (a.g.ny + TYR - 1) / TYR;
+  const unsigned int nb = (unsigned int)((long long)ntx * nty * a.g.nz);
+  k_spmv_tile<P, NC, KK, TYR><<<nb, 32 * TYR, bytes, s>>>(a, ntx, nty);
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) k_spmv_fin<KK><<<1, 1024, 0, s>>>(a, nb);
+  return true;
+}
+
+template <int P, int NC, int KK>
 static void launch_half(const SpmvArgs& a, cudaStream_t s) {
   constexpr int G = 8, BR = 32, WN = BR + 2 * P;
   constexpr size_t bytes = sizeof(double) * (2 * 2 * G * NC * WN * KK);
@@ -148,8 +277,9 @@ static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
     if (a.elastic) {
       if constexpr (NC == 3) launch_sm<P, 3, KK, true, 4>(a, (unsigned int)((nrb + 3) / 4), s);
     } else if (NC == 3) {
-      static int g3 = -1;  // warps per block of the 3-component (elastic) mass SpMV
-      if (g3 < 0) { const char* e = getenv("GA_SPMV_G3"); g3 = e ? atoi(e) : 8; }
+      static int g3 = -1;  // 3-component (elastic) mass SpMV: 0 row tiles (default), 4 / 8 warp row blocks
+      if (g3 < 0) { const char* e = getenv("GA_SPMV_G3"); g3 = e ? atoi(e) : 8; }  // tiles: opt-in (measured slower)
+      if (g3 == 0 && a.g.dim == 3 && launch_tile<P, NC, KK>(a, s)) return;
       if (g3 == 4) launch_sm<P, NC, KK, false, 4>(a, (unsigned int)((nrb + 3) / 4), s);
       else launch_sm<P, NC, KK, false, 8>(a, (unsigned int)((nrb + 7) / 8), s);
     } else {
