@@ -24,10 +24,11 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _ctx(cfg, dt):
+def _ctx(cfg, dt, op_mode=0):
     from paper_2102_11536_b200 import Context, make_desc
     prob = synth.make_problem(cfg)
-    desc = make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], k=cfg["k"], rho=cfg["rho"], dt=dt)
+    desc = make_desc(prob["patches"], cfg["p"], cfg["n"], cfg["dim"], k=cfg["k"], rho=cfg["rho"], dt=dt,
+                     op_mode=op_mode)
     return prob, Context(desc)
 
 
@@ -50,14 +51,17 @@ def test_c2_full_size_500_steps():
     assert max(errs) < 1e-10, errs
 
 
-def test_c3_p2_n192_sampled_rows_and_one_step():
+@pytest.mark.parametrize("op_mode", [1, 3, 2], ids=["stencil", "half_symmetric", "matrix_free"])
+def test_c3_p2_n192_sampled_rows_and_one_step(op_mode):
+    # every operator representation at the bench's largest grid (7.1 M DoFs)
     import torch
     cfg = synth.config("c3", p=2, n=192, k=2, rho=0.5)
     p, n, dim = cfg["p"], cfg["n"], 3
     m = n + p
     nf = m - 2
     dt = 2e-4
-    prob, ctx = _ctx(cfg, dt)
+    prob, ctx = _ctx(cfg, dt, op_mode)
+    assert ctx.operator_mode() == op_mode
     ctrl = prob["patches"][0][1]
     rng = np.random.default_rng(11)
     # free multi-indices: interior (1..m-2)^3; include faces/edges/corners of the free box
