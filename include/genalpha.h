@@ -162,6 +162,20 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
 ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const double* amp, const double* omega,
                          const double* phase, double t0, void* stream);
 
+/* Non-homogeneous Dirichlet data by lifting, single patch,
+ * scalar wave: the boundary control coefficients are U_b(t) = g_b h_D(t), h_D(t) = sum_{i<nterms}
+ * amp_i cos(omega_i t + phase_i), 1 <= nterms <= 4.  h_g: HOST array of all (n+p)^dim control
+ * values of the patch (co-lexicographic); only the boundary entries are used.  The free
+ * equations receive -M_fb g_b (h_D'' + a0 h_D') - K_fb g_b (h_D + a1 h_D') (C = a0 M + a1 K,
+ * ga_desc.damp_a0/a1) as two forcing pairs on top of ga_set_forcing's, with the same time origin
+ * t0 (set by ga_set_forcing, default 0); M_fb g_b and K_fb g_b are computed once on the GPU by
+ * the assembly (boundary columns).  The returned u, v, a are the free DoFs; the boundary values
+ * are g_b h_D(t).  d_scratch: >= ga_query's scratch_min bytes, released by the caller after the
+ * call.  h_g = NULL removes the lifting.  SYNCHRONIZES stream.  GA_ERR_ARG: multi-patch or
+ * elasticity, bad terms. */
+ga_status ga_set_dirichlet(ga_ctx* ctx, const double* h_g, int nterms, const double* amp, const double* omega,
+                           const double* phase, void* d_scratch, size_t scratch_bytes, void* stream);
+
 /* Advance nsteps explicit steps.  Asynchronous; a device-side
  * failure stops further steps and is reported by ga_get_stats. */
 ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream);

@@ -262,3 +262,23 @@ def operator_rows(ctrl, p, n, dim, rows, omega=1.0):
         cols = sorted(acc_M.keys(), key=lambda j: j[::-1])
         out[row] = (cols, np.array([acc_M[c] for c in cols]), np.array([acc_K[c] for c in cols]))
     return out
+
+
+def dirichlet_lift(ctrl, p, n, dim, g_full, hD_terms, a0=0.0, a1=0.0, omega=1.0):
+    """Non-homogeneous Dirichlet data by lifting, single patch,
+    scalar wave: the boundary control coefficients are U_b(t) = g_b h_D(t) (g_full: all m^d
+    control values, only the boundary entries are used; h_D = sum a cos(w t + phi)).  The free
+    equations M_ff U_f'' + C_ff U_f' + K_ff U_f = F_f - M_fb U_b'' - C_fb U_b' - K_fb U_b with
+    C = a0 M + a1 K become two forcing pairs: (-M_fb g_b) (h_D'' + a0 h_D') and
+    (-K_fb g_b) (h_D + a1 h_D').  Returns (GM, termsM, GK, termsK) for integrator.Forcing."""
+    from .integrator import sinusoid_derivative_terms
+    M, K = patch_operators(ctrl, p, n, dim, omega=omega)
+    m = n + p
+    free = interior_mask(m, dim)
+    bnd = ~free
+    gb = np.asarray(g_full, dtype=np.float64)[bnd]
+    GM = -(M[free][:, bnd] @ gb)
+    GK = -(K[free][:, bnd] @ gb)
+    termsM = sinusoid_derivative_terms(hD_terms, 2) + sinusoid_derivative_terms(hD_terms, 1, a0)
+    termsK = list(hD_terms) + sinusoid_derivative_terms(hD_terms, 1, a1)
+    return GM, termsM, GK, termsK

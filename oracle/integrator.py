@@ -79,6 +79,25 @@ class Forcing:
         return self.h(m, t) * self.G
 
 
+class ForcingSum:
+    """Sum of Forcing terms (e.g. a load plus the Dirichlet lifting pairs)."""
+
+    def __init__(self, parts):
+        self.parts = [f for f in parts if f is not None]
+
+    def __call__(self, m: int, t: float):
+        out = None
+        for f in self.parts:
+            v = f(m, t)
+            out = v if out is None else out + v
+        return out
+
+
+def sinusoid_derivative_terms(terms, order: int, scale: float = 1.0):
+    """Terms of scale * h^{(order)} for h = sum a cos(w t + phi): a w^order, w, phi + order pi/2."""
+    return [(scale * a * w ** order, w, ph + order * math.pi / 2) for a, w, ph in terms]
+
+
 def initial_chain(u0, v0, k: int, solve, Kop, F=None, t0: float = 0.0, Cop=None):
     """c_0 = U_0, c_1 = V_0, c_m = M^{-1}(F^{(m-2)}(t_0) - K c_{m-2} - C c_{m-1}), m = 2..3k-1."""
     c = [np.array(u0, dtype=np.float64), np.array(v0, dtype=np.float64)]

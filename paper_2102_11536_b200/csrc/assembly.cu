@@ -203,6 +203,26 @@ __global__ void k_contract_final(const double* __restrict__ in, const double* __
     if (gr[d] < 0 || gr[d] >= f.G[d]) return;
     if (gc[d] < 0 || gc[d] >= f.G[d]) gcol_ok = 0;
   }
+  if (f.bout) {
+    // boundary apply: only columns outside the free grid but inside the patch (boundary bases)
+    if (gcol_ok) return;
+    long long cl = 0, mul = 1;
+    for (int d = 0; d < DIM; ++d) {
+      const int cf = ii[d] + oo[d];  // patch-local full index of the column
+      if (cf < 0 || cf > m - 1) return;
+      cl += cf * mul;
+      mul *= m;
+    }
+    grow = gr[0] + (long long)f.G[0] * (gr[1] + (DIM == 3 ? (long long)f.G[1] * gr[2] : 0));
+    const int qs = max(0, i_out - f.p) * pp1, qe = (min(f.n - 1, i_out) + 1) * pp1;
+    const double* Ai = A + ((long long)i_out * W1 + o_out) * pp1 * pp1;
+    const double* src = in + ol * nlow_i + il;
+    const long long sq = nlow_o * nlow_i;
+    double sb = 0.0;
+    for (int q = qs; q < qe; ++q) sb = fma(__ldg(Ai + (q - qs)), __ldg(src + (long long)(q - f.qoff) * sq), sb);
+    atomicAdd(f.bout + grow, sb * f.bg[cl]);
+    return;
+  }
   if (!gcol_ok) return;
   grow = gr[0] + (long long)f.G[0] * (gr[1] + (DIM == 3 ? (long long)f.G[1] * gr[2] : 0));
   const long long gcol = gc[0] + (long long)f.G[0] * (gc[1] + (DIM == 3 ? (long long)f.G[1] * gc[2] : 0));

@@ -36,6 +36,10 @@ struct FinalDesc {
   const unsigned char* mask;
   int half;                    // half-symmetric layout: offsets o >= 0 only, rows shifted by hguard
   long long hguard;
+  // boundary apply (Dirichlet lifting): instead of storing coefficients, accumulate
+  // bout[row] += A(row, col) bg[col] over the boundary columns col (patch-local full index)
+  const double* bg;
+  double* bout;
 };
 
 void launch_geometry(const AsmPatch& P, int dim, int qa, int nqs, double* geo, long long gstride, double* minmax,

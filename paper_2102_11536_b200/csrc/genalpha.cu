@@ -83,10 +83,10 @@ struct ga_ctx {
   // forcing F = G h(t) (ga_set_forcing): grid vector, device slot table, host parameters
   double* forceG = nullptr;
   ForceSlots* fslots = nullptr;
-  bool forcing = false;
+  bool forcing = false;       // any pair active (pair 0 ga_set_forcing, 1-2 ga_set_dirichlet)
   double *lzv = nullptr, *lzab = nullptr;  // Lanczos vectors and alpha/beta (ga_lambda_max)
-  int fnterms = 0;
-  double famp[FMAXTERMS], fomega[FMAXTERMS], fphase[FMAXTERMS], ft0 = 0.0;
+  int fnterms[FMAXPAIRS] = {0, 0, 0};
+  double famp[FMAXPAIRS][FMAXTERMS], fomega[FMAXPAIRS][FMAXTERMS], fphase[FMAXPAIRS][FMAXTERMS], ft0 = 0.0;
   long long mfws = 0;    // Gauss points (n(p+1))^dim
   long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
 };
@@ -358,7 +358,7 @@ Layout make_layout(const Shape& sh) {
   L.off_partial = take(sizeof(double) * 2 * KMAX * maxblocks);
   L.off_counter = take(sizeof(unsigned int) * 16);
   L.off_dscal = take(sizeof(double) * 16);
-  L.off_forceG = take(sizeof(double) * sh.nvec * sh.g.padded);
+  L.off_forceG = take(sizeof(double) * FMAXPAIRS * sh.nvec * sh.g.padded);
   L.off_fslots = take(sizeof(ForceSlots));
   L.off_lz = take(sizeof(double) * 2 * sh.nvec * sh.g.padded * sh.k);  // Lanczos v_{j-1}, v_j (MV layout)
   L.off_lzab = take(sizeof(double) * 2 * (LZMAX + 2));
@@ -505,10 +505,16 @@ StageArgs stage_args(ga_ctx* c) {
 ForceArgs force_args(ga_ctx* c) {
   ForceArgs a;
   memset(&a, 0, sizeof(a));
-  a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.nterms = c->fnterms;
-  for (int i = 0; i < c->fnterms; ++i) { a.amp[i] = c->famp[i]; a.omega[i] = c->fomega[i]; a.phase[i] = c->fphase[i]; }
+  a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.npairs = FMAXPAIRS;
+  for (int r = 0; r < FMAXPAIRS; ++r) {
+    a.nterms[r] = c->fnterms[r];
+    a.G[r] = c->fnterms[r] > 0 ? c->forceG + (size_t)r * c->nvec * c->g.padded : nullptr;
+    for (int i = 0; i < c->fnterms[r]; ++i) {
+      a.amp[r][i] = c->famp[r][i]; a.omega[r][i] = c->fomega[r][i]; a.phase[r][i] = c->fphase[r][i];
+    }
+  }
   a.t0 = c->ft0; a.dt = c->d.dt;
-  a.G = c->forceG; a.b = c->b; a.slots = c->fslots; a.st = c->st;
+  a.b = c->b; a.slots = c->fslots; a.st = c->st;
   return a;
 }
 
@@ -596,7 +602,11 @@ ga_status build_graph(ga_ctx* ctx, cudaStream_t s, GraphKind kind, cudaGraph_t* 
 }
 
 // GPU assembly of M and K (sum factorisation, slab by slab).
-ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_bytes, cudaStream_t s) {
+// bg/boutM/boutK != null: boundary apply (Dirichlet lifting, ga_set_dirichlet): accumulate
+// M_fb bg and K_fb bg (free rows, boundary columns) into boutM/boutK instead of assembling.
+ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_bytes, cudaStream_t s,
+                   const double* bg = nullptr, double* boutM = nullptr, double* boutK = nullptr) {
+  const bool bapply = boutM != nullptr;
   const int dim = sh.dim, p = sh.p, n = sh.n, m = sh.m, W1 = sh.W1, pp1 = p + 1;
   const long long nq = (long long)n * pp1;
   Tables1D T = make_tables(p, n);
@@ -656,12 +666,12 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   const bool mfK = sh.mf && sh.nvec == 1;
   const long long Sh = (sh.S + 1) / 2, hrows = (sh.g.npts + sh.g.guard + 31) / 32 * 32;
   const size_t mbytes = sh.half ? sizeof(double) * Sh * hrows : sizeof(double) * sh.S * sh.g.cs;
-  if (!sh.mf) CK(cudaMemsetAsync(ctx->coefM, 0, mbytes, s));
-  if (!mfK) CK(cudaMemsetAsync(ctx->coefK, 0, sh.nvec == 3 ? sizeof(double) * sh.S * sh.g.cs * 9 : mbytes, s));
+  if (!sh.mf && !bapply) CK(cudaMemsetAsync(ctx->coefM, 0, mbytes, s));
+  if (!mfK && !bapply) CK(cudaMemsetAsync(ctx->coefK, 0, sh.nvec == 3 ? sizeof(double) * sh.S * sh.g.cs * 9 : mbytes, s));
   // term list: (target block pointer, spec, derivative flags per direction)
   struct Term { double* coef; TermSpec ts; int sflag[3], tflag[3]; int ab; };
   std::vector<Term> terms;
-  if (!sh.mf) {
+  if (!sh.mf || bapply) {
     Term t;
     memset(&t, 0, sizeof(t));
     t.coef = ctx->coefM;
@@ -669,7 +679,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
     t.ts.scale = sh.nvec == 3 ? ctx->d.density : 1.0;
     terms.push_back(t);
   }
-  if (sh.nvec == 1 && !mfK) {
+  if (sh.nvec == 1 && (!mfK || bapply)) {
     for (int c = 0; c < dim; ++c)
       for (int e = 0; e < dim; ++e) {
         Term t;
@@ -704,7 +714,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
       const int qa = ea * pp1, nqs = (eb - ea) * pp1;
       const long long npts_s = lowpts * nqs;
       launch_geometry(P, dim, qa, nqs, geo, npts_s, dmin, s);
-      if (sh.mf) {
+      if (sh.mf && !bapply) {
         // Gauss-point data of the matrix-free operators for quadrature planes [qa, qa + nqs)
         // (overlapping slabs rewrite identical values): W_M = density w|J|, and for the scalar
         // K the symmetric omega^2 w|J| (J^-1 J^-T)_{ce}, c <= e (SoA, stride mfws)
@@ -748,6 +758,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         f.mask = ctx->mask;
         f.half = (sh.half && f.ncf == 1) ? 1 : 0;  // the elastic K stays full
         f.hguard = sh.g.guard;
+        if (bapply) { f.bg = bg; f.bout = (t.coef == ctx->coefM) ? boutM : boutK; }
         if (dim == 3) {
           ContractDesc c2;
           memset(&c2, 0, sizeof(c2));
@@ -1175,31 +1186,11 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
   return set_predictors_and_norm(ctx, s);
 }
 
-ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const double* amp, const double* omega,
-                         const double* phase, double t0, void* stream) {
-  ga_status rc = check_ctx(ctx);
-  if (rc != GA_OK) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool on = d_G != nullptr && nterms > 0;
-  if (on && (nterms > FMAXTERMS || !amp || !omega || !phase)) {
-    seterr(ctx, "forcing: 1..8 terms with amp, omega and phase arrays required");
-    return GA_ERR_ARG;
-  }
-  for (int i = 0; on && i < nterms; ++i)
-    if (!std::isfinite(amp[i]) || !std::isfinite(omega[i]) || !std::isfinite(phase[i])) {
-      seterr(ctx, "forcing: non-finite term");
-      return GA_ERR_ARG;
-    }
-  ctx->forcing = on;
-  ctx->fnterms = on ? nterms : 0;
-  ctx->ft0 = t0;
-  for (int i = 0; i < ctx->fnterms; ++i) { ctx->famp[i] = amp[i]; ctx->fomega[i] = omega[i]; ctx->fphase[i] = phase[i]; }
-  if (on) {
-    CK(cudaMemsetAsync(ctx->forceG, 0, sizeof(double) * ctx->nvec * ctx->g.padded, s));
-    launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_G, ctx->forceG, 1, 0, ctx->st, s);
-    CK(cudaGetLastError());
-  }
-  // the captured graphs carry the forcing kernel (and its parameters): rebuild them
+// (re)capture the graphs after a change of the forcing pairs and refresh the step slots
+static ga_status rebuild_forcing_graphs(ga_ctx* ctx, cudaStream_t s) {
+  ga_status rc = GA_OK;
+  ctx->forcing = false;
+  for (int r = 0; r < FMAXPAIRS; ++r) ctx->forcing |= ctx->fnterms[r] > 0;
   CK(cudaStreamSynchronize(s));
   if (!ctx->nograph) {
     cudaGraphExec_t* ex[3] = {&ctx->g_step, &ctx->g_solveK, &ctx->g_solveB};
@@ -1215,6 +1206,85 @@ ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const doubl
     if (rc != GA_OK) return rc;
   }
   return set_step_slots(ctx, s);
+}
+
+ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const double* amp, const double* omega,
+                         const double* phase, double t0, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool on = d_G != nullptr && nterms > 0;
+  if (on && (nterms > FMAXTERMS || !amp || !omega || !phase)) {
+    seterr(ctx, "forcing: 1..8 terms with amp, omega and phase arrays required");
+    return GA_ERR_ARG;
+  }
+  for (int i = 0; on && i < nterms; ++i)
+    if (!std::isfinite(amp[i]) || !std::isfinite(omega[i]) || !std::isfinite(phase[i])) {
+      seterr(ctx, "forcing: non-finite term");
+      return GA_ERR_ARG;
+    }
+  ctx->fnterms[0] = on ? nterms : 0;
+  ctx->ft0 = t0;
+  for (int i = 0; i < ctx->fnterms[0]; ++i) { ctx->famp[0][i] = amp[i]; ctx->fomega[0][i] = omega[i]; ctx->fphase[0][i] = phase[i]; }
+  if (on) {
+    CK(cudaMemsetAsync(ctx->forceG, 0, sizeof(double) * ctx->nvec * ctx->g.padded, s));
+    launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_G, ctx->forceG, 1, 0, ctx->st, s);
+    CK(cudaGetLastError());
+  }
+  return rebuild_forcing_graphs(ctx, s);
+}
+
+ga_status ga_set_dirichlet(ga_ctx* ctx, const double* h_g, int nterms, const double* amp, const double* omega,
+                           const double* phase, void* d_scratch, size_t scratch_bytes, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool on = h_g != nullptr && nterms > 0;
+  if (on && (ctx->patches.size() != 1 || ctx->nvec != 1)) {
+    seterr(ctx, "Dirichlet lifting: single patch, scalar wave only");
+    return GA_ERR_ARG;
+  }
+  if (on && (2 * nterms > FMAXTERMS || !amp || !omega || !phase || !d_scratch)) {
+    seterr(ctx, "Dirichlet lifting: 1..4 terms, amp/omega/phase and scratch required");
+    return GA_ERR_ARG;
+  }
+  for (int i = 0; on && i < nterms; ++i)
+    if (!std::isfinite(amp[i]) || !std::isfinite(omega[i]) || !std::isfinite(phase[i])) {
+      seterr(ctx, "Dirichlet lifting: non-finite term");
+      return GA_ERR_ARG;
+    }
+  ctx->fnterms[1] = ctx->fnterms[2] = 0;
+  if (on) {
+    // boundary apply: M_fb g and K_fb g by the assembly's last contraction (free rows, boundary
+    // columns) into the pair-1/2 load vectors; the pairs carry the signs:
+    //   pair 1: -(M_fb g) (h'' + a0 h'),  pair 2: -(K_fb g) (h + a1 h')   (R16)
+    const long long mpow = ctx->dim == 3 ? (long long)ctx->m * ctx->m * ctx->m : (long long)ctx->m * ctx->m;
+    const size_t gbytes = (sizeof(double) * mpow + 255) & ~(size_t)255;
+    if (scratch_bytes < gbytes) { seterr(ctx, "scratch too small"); return GA_ERR_OOM; }
+    double* dg = (double*)d_scratch;
+    CK(cudaMemcpyAsync(dg, h_g, sizeof(double) * mpow, cudaMemcpyHostToDevice, s));
+    const size_t vb = sizeof(double) * ctx->nvec * ctx->g.padded;
+    double* GM = ctx->forceG + ctx->nvec * ctx->g.padded;
+    double* GK = GM + ctx->nvec * ctx->g.padded;
+    CK(cudaMemsetAsync(GM, 0, 2 * vb, s));
+    Shape sh;
+    sh.dim = ctx->dim; sh.nvec = ctx->nvec; sh.p = ctx->p; sh.n = ctx->n; sh.m = ctx->m; sh.k = ctx->k;
+    sh.W1 = ctx->W1; sh.S = ctx->S; sh.g = ctx->g; sh.nfree = ctx->nfree; sh.mf = ctx->mf; sh.half = ctx->half;
+    rc = assemble(ctx, sh, (char*)d_scratch + gbytes, scratch_bytes - gbytes, s, dg, GM + ctx->g.guard,
+                  GK + ctx->g.guard);
+    if (rc != GA_OK) return rc;
+    const double a0 = ctx->d.damp_a0, a1 = ctx->d.damp_a1;
+    int n1 = 0, n2 = 0;
+    for (int i = 0; i < nterms; ++i) {
+      const double a = amp[i], w = omega[i], ph = phase[i];
+      ctx->famp[1][n1] = -a * w * w; ctx->fomega[1][n1] = w; ctx->fphase[1][n1++] = ph + 3.141592653589793;
+      ctx->famp[1][n1] = -a0 * a * w; ctx->fomega[1][n1] = w; ctx->fphase[1][n1++] = ph + 1.5707963267948966;
+      ctx->famp[2][n2] = -a; ctx->fomega[2][n2] = w; ctx->fphase[2][n2++] = ph;
+      ctx->famp[2][n2] = -a1 * a * w; ctx->fomega[2][n2] = w; ctx->fphase[2][n2++] = ph + 1.5707963267948966;
+    }
+    ctx->fnterms[1] = n1; ctx->fnterms[2] = n2;
+  }
+  return rebuild_forcing_graphs(ctx, s);
 }
 
 ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream) {

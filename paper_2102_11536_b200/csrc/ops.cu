@@ -1044,26 +1044,38 @@ __global__ void __launch_bounds__(NTHREADS) k_add_forcing(ForceArgs a) {
   if (a.st->status != 0) return;
   count_launch(const_cast<DevStatus*>(a.st));
   const GridDesc g = a.g;
-  // h^{(m)}(t) per slot, identical in every thread (computed redundantly: a few terms)
-  double hj[KK];
+  // h_r^{(m)}(t) per pair and slot, identical in every thread (a few terms, computed redundantly)
+  double hj[FMAXPAIRS][KK];
   const double tn = a.t0 + (double)a.st->steps * a.dt;
 #pragma unroll
-  for (int j = 0; j < KK; ++j) {
-    double h = 0.0;
-    if (a.slots->active[j]) {
-      const int m = a.slots->order[j];
-      const double t = tn + a.slots->toff[j];
-      for (int i = 0; i < a.nterms; ++i) h += a.amp[i] * pow(a.omega[i], (double)m) * cos(a.omega[i] * t + a.phase[i] + m * 1.5707963267948966);
+  for (int r = 0; r < FMAXPAIRS; ++r)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      double h = 0.0;
+      if (r < a.npairs && a.slots->active[j]) {
+        const int m = a.slots->order[j];
+        const double t = tn + a.slots->toff[j];
+        for (int i = 0; i < a.nterms[r]; ++i)
+          h += a.amp[r][i] * pow(a.omega[r][i], (double)m) * cos(a.omega[r][i] * t + a.phase[r][i] + m * 1.5707963267948966);
+      }
+      hj[r][j] = h;
     }
-    hj[j] = h;
-  }
   const long long tot = (long long)a.nvec * g.npts;
   for (long long e = (long long)gtid(); e < tot; e += (long long)gridDim.x * blockDim.x) {
     const long long c = e / g.npts, i = e - c * g.npts;
     const long long gi = c * g.padded + g.guard + i;
-    const double G = a.G[gi];
+    double add[KK];
 #pragma unroll
-    for (int j = 0; j < KK; ++j) a.b[gi * KK + j] = fma(hj[j], G, a.b[gi * KK + j]);
+    for (int j = 0; j < KK; ++j) add[j] = 0.0;
+#pragma unroll
+    for (int r = 0; r < FMAXPAIRS; ++r) {
+      if (r >= a.npairs || !a.G[r]) continue;
+      const double G = a.G[r][gi];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) add[j] = fma(hj[r][j], G, add[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < KK; ++j) a.b[gi * KK + j] += add[j];
   }
 }
 

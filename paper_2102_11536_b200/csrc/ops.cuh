@@ -127,6 +127,7 @@ void launch_stage(const StageArgs& a, cudaStream_t s);
 // table lives on the device (written before each solve set: the initial chain uses orders m-2 at
 // t0, the step orders 3j at t_n + alpha_fj dt), so the captured graphs need no rebuild.
 constexpr int FMAXTERMS = 8;
+constexpr int FMAXPAIRS = 3;  // pair 0: ga_set_forcing; pairs 1, 2: Dirichlet lifting (ga_set_dirichlet)
 struct ForceSlots {
   int active[KMAX];
   int order[KMAX];
@@ -134,10 +135,11 @@ struct ForceSlots {
 };
 struct ForceArgs {
   GridDesc g;
-  int nvec, kk, nterms;
-  double amp[FMAXTERMS], omega[FMAXTERMS], phase[FMAXTERMS];
+  int nvec, kk, npairs;
+  int nterms[FMAXPAIRS];
+  double amp[FMAXPAIRS][FMAXTERMS], omega[FMAXPAIRS][FMAXTERMS], phase[FMAXPAIRS][FMAXTERMS];
   double t0, dt;
-  const double* G;           // grid vector [c][guard | npts | guard]
+  const double* G[FMAXPAIRS];  // grid vectors [c][guard | npts | guard] (b += sum_pairs h^{(m)} G)
   double* b;                 // MV [c][guard | npts | guard][kk]
   const ForceSlots* slots;   // device
   const DevStatus* st;       // st->steps: completed steps since ga_set_state

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
                 -4: "GA_ERR_CONFORMITY", -5: "GA_ERR_NOCONV", -6: "GA_ERR_UNSTABLE",
                 -7: "GA_ERR_CUDA", -8: "GA_ERR_OOM"}
 
-EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_advance", "ga_get_state",
+EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_set_dirichlet", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
             "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_operator_mode", "ga_destroy",
             "ga_last_error"]
@@ -68,6 +68,7 @@ def _load():
         "ga_set_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
         "ga_advance": (c_int, [c_void_p, c_int, c_void_p]),
         "ga_set_forcing": (c_int, [c_void_p, c_void_p, c_int, P, P, P, c_double, c_void_p]),
+        "ga_set_dirichlet": (c_int, [c_void_p, P, c_int, P, P, P, c_void_p, c_size_t, c_void_p]),
         "ga_get_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
         "ga_get_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
         "ga_set_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
@@ -189,6 +190,24 @@ class Context:
         arr = [(c_double * max(1, n))(*[t[i] for t in terms]) for i in range(3)]
         _check(lib.ga_set_forcing(self.ctx, _ptr(G) if G is not None else None, n, arr[0], arr[1], arr[2],
                                   float(t0), self._s()), self.ctx)
+
+    def set_dirichlet(self, g=None, terms=()):
+        """Boundary values U_b(t) = g_b h_D(t), h_D = sum a cos(w t + phi) for (a, w, phi) in terms;
+        g: numpy array of all (n+p)^dim control values of the (single) patch, None removes it."""
+        import numpy as _np
+        torch = self.torch
+        n = len(terms) if g is not None else 0
+        arr = [(c_double * max(1, n))(*[t[i] for t in terms]) for i in range(3)]
+        gp = None
+        if g is not None:
+            gc = _np.ascontiguousarray(g, dtype=_np.float64)
+            gp = gc.ctypes.data_as(POINTER(c_double))
+        _, _, sc, smin = ga_query(self.desc)
+        sc += 8 * (self.desc.n + self.desc.p) ** self.desc.dim + 512  # + the uploaded control values
+        scratch = torch.empty(sc + 256, dtype=torch.uint8, device=self.workspace.device)
+        _check(lib.ga_set_dirichlet(self.ctx, gp, n, arr[0], arr[1], arr[2], _aligned(scratch), sc, self._s()),
+               self.ctx)
+        del scratch
 
     def advance(self, nsteps):
         _check(lib.ga_advance(self.ctx, int(nsteps), self._s()), self.ctx)

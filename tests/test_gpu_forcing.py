@@ -126,3 +126,69 @@ def test_rayleigh_damping_parity(cfg, op_mode, forced):
     ref = it.run(u0, v0, nsteps)
     errs = [mnorm_rel(d.M, x, y) for x, y in zip(got, ref[:3])]
     assert max(errs) < 1e-10, errs
+
+
+def _lift_case(p, n, k, rho, dt, a0=0.0, a1=0.0, noise=0.0, seed=3):
+    import torch
+
+    from paper_2102_11536_b200 import Context, make_desc
+    ctrl = synth.control_net(2, p, n, noise=noise, seed=seed)
+    desc = make_desc([((0, 0), ctrl)], p, n, 2, k=k, rho=rho, dt=dt, damp_a0=a0, damp_a1=a1)
+    return ctrl, Context(desc), torch
+
+
+@pytest.mark.parametrize("a0,a1,forced", [(0.0, 0.0, False), (0.5, 0.002, True)])
+def test_dirichlet_lifting_parity(a0, a1, forced):
+    # S:230-239 lifting on a deformed patch: boundary values g_b h_D(t); GPU = oracle (dirichlet_lift)
+    p, n, k, rho, dt, nsteps = 3, 10, 2, 0.5, 2e-3, 20
+    ctrl, ctx, torch = _lift_case(p, n, k, rho, dt, a0, a1, noise=0.2)
+    m = n + p
+    g = np.cos(1.3 * ctrl[:, 0]) + ctrl[:, 1] ** 2  # any boundary data (interior entries unused)
+    hD = [(1.0, 4.0, 0.2), (0.4, 7.0, -1.0)]
+    d = assembly.Discretization([((0, 0), ctrl)], p, n, 2)
+    free = assembly.interior_mask(m, 2)
+    parts = []
+    if forced:
+        G = d.M @ np.cos(np.arange(d.nfree) * 0.37)
+        ctx.set_forcing(torch.tensor(G, device="cuda"), TERMS, 0.0)
+        parts.append(integrator.Forcing(G, TERMS))
+    ctx.set_dirichlet(g, hD)
+    GM, tM, GK, tK = assembly.dirichlet_lift(ctrl, p, n, 2, g, hD, a0, a1)
+    parts += [integrator.Forcing(GM, tM), integrator.Forcing(GK, tK)]
+    u0 = np.sin(np.arange(d.nfree) * 0.1)
+    ctx.set_state(torch.tensor(u0, device="cuda"))
+    ctx.advance(nsteps)
+    assert ctx.stats().status == 0
+    got = [t.cpu().numpy() for t in ctx.get_state()]
+    C = a0 * d.M + a1 * d.K if (a0 or a1) else None
+    ref = integrator.Integrator(d.M, d.K, k, rho, dt, forcing=integrator.ForcingSum(parts), C=C).run(
+        u0, np.zeros(d.nfree), nsteps)
+    errs = [mnorm_rel(d.M, x, y) for x, y in zip(got, ref[:3])]
+    assert max(errs) < 1e-10, errs
+    # removing the lifting restores the homogeneous problem (forcing kept)
+    ctx.set_dirichlet(None)
+    ctx.set_state(torch.tensor(u0, device="cuda"))
+    ctx.advance(3)
+    ref2 = integrator.Integrator(d.M, d.K, k, rho, dt, forcing=parts[0] if forced else None, C=C).run(
+        u0, np.zeros(d.nfree), 3)
+    assert mnorm_rel(d.M, ctx.get_state()[0].cpu().numpy(), ref2[0]) < 1e-10
+
+
+def test_dirichlet_lifting_exact_in_space_order():
+    # u = (1 + x + 2y) cos(2t) lies in the spline space on the identity map: the GPU error at
+    # t = 1 is the time discretisation only, order 2k = 4 (k = 2)
+    p, n, k = 2, 8, 2
+    errs = []
+    for tau in (0.04, 0.02, 0.01):
+        ctrl, ctx, torch = _lift_case(p, n, k, 0.5, tau)
+        free = assembly.interior_mask(n + p, 2)
+        L = 1.0 + ctrl[:, 0] + 2.0 * ctrl[:, 1]
+        Mfull, _ = assembly.patch_operators(ctrl, p, n, 2)
+        ctx.set_forcing(torch.tensor((Mfull @ L)[free], device="cuda"), [(-4.0, 2.0, 0.0)], 0.0)
+        ctx.set_dirichlet(L, [(1.0, 2.0, 0.0)])
+        ctx.set_state(torch.tensor(L[free], device="cuda"))
+        ctx.advance(int(round(1.0 / tau)))
+        assert ctx.stats().status == 0
+        errs.append(np.abs(ctx.get_state()[0].cpu().numpy() - L[free] * math.cos(2.0)).max())
+    o = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert o[-1] > 2 * k - 0.3, (o, errs)

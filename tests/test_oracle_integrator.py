@@ -241,3 +241,33 @@ def test_damped_scalar_ode_order_2k(k):
         errs.append(e)
     o = _orders(errs)
     assert o[-1] > 2 * k - 0.35, (o, errs)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_dirichlet_lift_exact_in_space(k):
+    # Lifting: u = L(x, y) cos(2t), L = 1 + x + 2y, solves u_tt - Laplace u = f with
+    # f = -4 L cos(2t) and u = L cos(2t) on the boundary.  On the identity map L lies in the spline
+    # space (Greville control values reproduce linear functions), so the semi-discrete solution is
+    # exact and the error is the time discretisation only: order 2k (with Rayleigh damping too).
+    p, n = 2, 6
+    ctrl = synth.control_net(2, p, n)
+    Lc = 1.0 + ctrl[:, 0] + 2.0 * ctrl[:, 1]
+    d = assembly.Discretization([((0, 0), ctrl)], p, n, 2)
+    free = assembly.interior_mask(n + p, 2)
+    Mfull, _ = assembly.patch_operators(ctrl, p, n, 2)
+    hD = [(1.0, 2.0, 0.0)]
+    for a0, a1 in ((0.0, 0.0), (0.7, 0.01)):
+        # f = u_tt + C-term - Laplace u: with damping C = a0 M + a1 K the exact u needs
+        # f = L (-4 cos 2t) + a0 L (-2 sin 2t) (K L = 0 up to the boundary: lifting handles it)
+        GM, tM, GK, tK = assembly.dirichlet_lift(ctrl, p, n, 2, Lc, hD, a0, a1)
+        Gf = (Mfull @ Lc)[free]  # int L B_i over free i (M applied to the exact coefficients)
+        tf = [(-4.0, 2.0, 0.0), (2.0 * a0, 2.0, math.pi / 2)]
+        F = integrator.ForcingSum([integrator.Forcing(Gf, tf), integrator.Forcing(GM, tM), integrator.Forcing(GK, tK)])
+        C = a0 * d.M + a1 * d.K if (a0 or a1) else None
+        errs = []
+        for tau in (0.04, 0.02, 0.01):
+            it = integrator.Integrator(d.M, d.K, k, 0.5, tau, forcing=F, C=C)
+            c = it.run(Lc[free], np.zeros(d.nfree), int(round(1.0 / tau)))
+            errs.append(np.abs(c[0] - Lc[free] * math.cos(2.0)).max())
+        o = _orders(errs)
+        assert o[-1] > 2 * k - 0.3, (a0, a1, o, errs)
