@@ -129,6 +129,14 @@ ga_status ga_params(int k, double rho_b, double rho_s, int param_set,
                     double* alpha, double* beta, double* gamma, double* alpha_f,
                     double* theta_max);
 
+/* Spectral radius rho(G(Theta)) of the amplification matrix for n values Theta = tau^2 lambda
+ * (Figs. 1-2): d_theta, d_rho device arrays of n doubles; G is
+ * block upper triangular with the 3x3 blocks Lambda_j of the same parameters as
+ * ga_params, so rho(G) = max_j of the largest root of det(mu - Lambda_j) (closed-form cubic).
+ * Asynchronous on stream, no context needed.  GA_ERR_PARAM on bad rho. */
+ga_status ga_spectral_scan(int k, double rho_b, double rho_s, int param_set, const double* d_theta, int n,
+                           double* d_rho, void* stream);
+
 /* Sizes for a descriptor (host only, no GPU).  n_free: length of a free-DoF
  * vector (= ncomp * scalar free DoFs).  workspace_bytes: device memory the
  * context keeps for its lifetime.  scratch_bytes: device memory needed only

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
                 -4: "GA_ERR_CONFORMITY", -5: "GA_ERR_NOCONV", -6: "GA_ERR_UNSTABLE",
                 -7: "GA_ERR_CUDA", -8: "GA_ERR_OOM"}
 
-EXPORTED = ["ga_params", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_set_dirichlet", "ga_advance", "ga_get_state",
+EXPORTED = ["ga_params", "ga_spectral_scan", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_set_dirichlet", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
             "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_operator_mode", "ga_destroy",
             "ga_last_error"]
@@ -63,6 +63,7 @@ def _load():
     P, D = POINTER(c_double), POINTER(ga_desc)
     sig = {
         "ga_params": (c_int, [c_int, c_double, c_double, c_int, P, P, P, P, P]),
+        "ga_spectral_scan": (c_int, [c_int, c_double, c_double, c_int, c_void_p, c_int, c_void_p, c_void_p]),
         "ga_query": (c_int, [D, POINTER(c_size_t), POINTER(c_size_t), POINTER(c_size_t), POINTER(c_size_t)]),
         "ga_create": (c_int, [D, c_void_p, c_size_t, c_void_p, c_size_t, c_void_p, POINTER(c_void_p)]),
         "ga_set_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -110,6 +111,17 @@ def ga_params(k, rho_b, rho_s=None, param_set=0):
     th = c_double()
     _check(lib.ga_params(k, rho_b, rho_s, param_set, *arr, byref(th)))
     return tuple(np.array(a[:k]) for a in arr) + (th.value,)
+
+
+def spectral_scan(theta, k, rho_b, rho_s=None, param_set=0):
+    """rho(G(Theta)) for a CUDA float64 tensor of Theta values (ga_spectral_scan)."""
+    import torch
+    rho_s = rho_b if rho_s is None else rho_s
+    th = theta.contiguous()
+    out = torch.empty_like(th)
+    _check(lib.ga_spectral_scan(int(k), float(rho_b), float(rho_s), int(param_set), c_void_p(th.data_ptr()),
+                                th.numel(), c_void_p(out.data_ptr()), c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out
 
 
 def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3, param_set=0,
