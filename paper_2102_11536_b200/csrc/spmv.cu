@@ -234,7 +234,7 @@ static void launch_sm(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
 
 template <int P, int NC, int KK>
 static bool launch_tile(const SpmvArgs& a, cudaStream_t s) {
-  constexpr int TYR = 4, TX = 32 + 2 * P, TY = TYR + 2 * P;
+  constexpr int TYR = 8, TX = 32 + 2 * P, TY = TYR + 2 * P;
   constexpr size_t bytes = sizeof(double) * 2 * TY * TX * NC * KK;
   if (bytes > 200 * 1024) return false;
   static bool attr = false;
