@@ -173,6 +173,153 @@ __global__ void __launch_bounds__(32 * TYR) k_spmv_tile(SpmvArgs a, int ntx, int
   }
 }
 
+// Register-blocked row tiles for the 3-component mass SpMV (the elastic M = density * scalar M
+// per component).  The warp-per-row-block kernel reads
+// W * NC * KK window values from shared memory per row and offset line (54 at NC = 3, KK = 2)
+// against W coefficients from HBM: shared-memory bandwidth, not HBM, binds it.  Here a CTA of
+// TYW warps owns a 32 (x) x TYW R (y) tile at one z; per z offset o3 it stages the
+// (TYW R + 2P) y-lines x (32 + 2P) points x NC x KK input plane once (cp.async 16 B,
+// double-buffered), and each thread computes R rows (x, y .. y + R - 1): every staged value is
+// read once from shared memory and used for the up to R rows whose y offset reaches it, with
+// that row's coefficient c(row, o3, o2 = t - r, o1) held in registers.  Shared-memory reads per
+// row and line drop by R W / (R + 2P) (3x at P = 4, R = 4).  Staged lines past ny - 1 + P are
+// only read by rows outside the grid and are zero-filled (no load beyond the guard).
+template <int P, int NC, int KK, int TYW, int R>
+__global__ void __launch_bounds__(32 * TYW, 2) k_spmv_rt(SpmvArgs a, int ntx, int nty) {
+  constexpr int W = 2 * P + 1, TX = 32 + 2 * P, TYR = TYW * R, TY = TYR + 2 * P, V = NC * KK;
+  constexpr int PLANE = TY * TX * V;
+  constexpr int NT = 32 * TYW;
+  constexpr int U = (KK % 2 == 0) ? 2 : 1;  // doubles per cp.async
+  if (a.st->status != 0 && a.mode != SPMV_APPLY) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.st->launches, 1ull);
+  extern __shared__ __align__(16) double smem_rt[];
+  double* buf0 = smem_rt;
+  double* buf1 = smem_rt + PLANE;
+  const GridDesc g = a.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = blockIdx.x % ntx;
+  const int ty = (blockIdx.x / ntx) % nty;
+  const int z = blockIdx.x / (ntx * nty);
+  const int x0 = tx * 32, y0 = ty * TYR;
+  const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+  const int x = x0 + lane, yw = y0 + w * R;
+  const long long S = (long long)W * W * W;
+  const double* cs[R];
+  bool valid[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    valid[r] = x < g.nx && yw + r < g.ny;
+    const long long i = x + sy * (yw + r) + sz * z;
+    const long long icl = valid[r] ? i : 0;
+    cs[r] = a.coef + (icl >> 5) * S * 32 + (icl & 31);
+  }
+  const int ylim = g.ny - 1 + P;
+  auto issue_plane = [&](int o3, double* dst) {
+    for (int q = threadIdx.x; q < PLANE / U; q += NT) {
+      const int e = q * U;
+      const int j = e % KK, c = (e / KK) % NC, txp = (e / V) % TX, typ = e / (V * TX);
+      const int yy = y0 - P + typ;
+      if (yy <= ylim) {
+        const long long pos = g.guard + (x0 - P + txp) + sy * yy + sz * (z + o3);
+        const unsigned int d = (unsigned int)__cvta_generic_to_shared(dst + e);
+        const double* src = a.x + ((long long)c * g.padded + pos) * KK + j;
+        if constexpr (U == 2)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+      } else {
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) dst[e + uu] = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double acc[R][V];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[r][v] = 0.0;
+  issue_plane(-P, buf0);
+#pragma unroll 1
+  for (int o3i = 0; o3i < W; ++o3i) {
+    double* cur = (o3i & 1) ? buf1 : buf0;
+    double* nxt = (o3i & 1) ? buf0 : buf1;
+    if (o3i + 1 < W) {
+      issue_plane(o3i + 1 - P, nxt);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const long long lbase = (long long)o3i * W * W * 32;
+#pragma unroll
+    for (int t = 0; t < R + 2 * P; ++t) {
+      double cc[R][W];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int o2i = t - r;
+        if (o2i >= 0 && o2i < W) {
+#pragma unroll
+          for (int u = 0; u < W; ++u) cc[r][u] = __ldg(cs[r] + lbase + (long long)(o2i * W + u) * 32);
+        }
+      }
+      const double* row = cur + ((w * R + t) * TX + lane) * V;
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        double v[V];
+        if constexpr (V % 2 == 0) {
+#pragma unroll
+          for (int h = 0; h < V / 2; ++h) {
+            const double2 t2 = *reinterpret_cast<const double2*>(row + u * V + 2 * h);
+            v[2 * h] = t2.x; v[2 * h + 1] = t2.y;
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < V; ++h) v[h] = row[u * V + h];
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int o2i = t - r;
+          if (o2i >= 0 && o2i < W) {
+#pragma unroll
+            for (int h = 0; h < V; ++h) acc[r][h] = fma(cc[r][u], v[h], acc[r][h]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with cur before it is refilled
+  }
+  double dots[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) dots[j] = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (!valid[r]) continue;
+    const long long i = x + sy * (yw + r) + sz * z;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+      double pv[KK];
+      if (a.mode == SPMV_PQ) load_row<KK>(a.x + base, pv);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        double v = acc[r][c * KK + j];
+        if (a.mode == SPMV_NEGB) v = -v;
+        else if (a.mode == SPMV_TRUERES) { v = a.b[base + j] - v; dots[j] = fma(v, v, dots[j]); }
+        else if (a.mode == SPMV_PQ) dots[j] = fma(pv[j], v, dots[j]);
+        a.y[base + j] = v;
+      }
+    }
+  }
+  if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) {
+    block_sum<KK>(dots);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < KK; ++j) a.partial[(size_t)blockIdx.x * KK + j] = dots[j];
+    }
+  }
+}
+
 // Fixed-order sum of the SpMV block partials and the PCG scalar step:
 // SPMV_PQ: alpha_j = r.z / p.q (F2); SPMV_TRUERES: restart of the refinement phase.
 template <int KK>
@@ -251,6 +398,30 @@ static bool launch_tile(const SpmvArgs& a, cudaStream_t s) {
   return true;
 }
 
+template <int P, int NC, int KK, int TYW, int R>
+static bool launch_rt(const SpmvArgs& a, cudaStream_t s) {
+  constexpr int TX = 32 + 2 * P, TY = TYW * R + 2 * P;
+  constexpr size_t bytes = sizeof(double) * 2 * TY * TX * NC * KK;
+  if constexpr (bytes > 200 * 1024) {
+    return false;
+  } else {
+    // one block per 32 x TYW R tile: never more blocks than 32-row blocks (partial slots)
+    if (a.g.dim != 3 || a.g.nx < 32 || a.g.ny < TYW * R) return false;
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(k_spmv_rt<P, NC, KK, TYW, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)bytes) != cudaSuccess)
+        return false;
+      attr = true;
+    }
+    const int ntx = (a.g.nx + 31) / 32, nty = (a.g.ny + TYW * R - 1) / (TYW * R);
+    const unsigned int nb = (unsigned int)((long long)ntx * nty * a.g.nz);
+    k_spmv_rt<P, NC, KK, TYW, R><<<nb, 32 * TYW, bytes, s>>>(a, ntx, nty);
+    if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) k_spmv_fin<KK><<<1, 1024, 0, s>>>(a, nb);
+    return true;
+  }
+}
+
 template <int P, int NC, int KK>
 static void launch_half(const SpmvArgs& a, cudaStream_t s) {
   constexpr int G = 8, BR = 32, WN = BR + 2 * P;
@@ -279,6 +450,12 @@ static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
     } else if (NC == 3) {
       static int g3 = -1;  // 3-component (elastic) mass SpMV: 0 row tiles (default), 4 / 8 warp row blocks
       if (g3 < 0) { const char* e = getenv("GA_SPMV_G3"); g3 = e ? atoi(e) : 8; }  // tiles: opt-in (measured slower)
+      static int rt = -1;  // register-blocked row tiles (default 4 x 4; C4 M apply 1.48 -> 1.24 ms, 8 x 2: 1.33)
+      if (rt < 0) { const char* e = getenv("GA_SPMV_RT"); rt = e ? atoi(e) : 1; }
+      if constexpr (NC == 3) {
+        if (rt == 1 && launch_rt<P, NC, KK, 4, 4>(a, s)) return;  // 4 warps x 4 rows, 2 CTAs / SM
+        if (rt == 2 && launch_rt<P, NC, KK, 8, 2>(a, s)) return;  // 8 warps x 2 rows, 2 CTAs / SM
+      }
       if (g3 == 0 && a.g.dim == 3 && launch_tile<P, NC, KK>(a, s)) return;
       if (g3 == 4) launch_sm<P, NC, KK, false, 4>(a, (unsigned int)((nrb + 3) / 4), s);
       else launch_sm<P, NC, KK, false, 8>(a, (unsigned int)((nrb + 7) / 8), s);
