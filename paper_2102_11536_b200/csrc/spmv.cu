@@ -184,8 +184,8 @@ __global__ void __launch_bounds__(32 * TYR) k_spmv_tile(SpmvArgs a, int ntx, int
 // that row's coefficient c(row, o3, o2 = t - r, o1) held in registers.  Shared-memory reads per
 // row and line drop by R W / (R + 2P) (3x at P = 4, R = 4).  Staged lines past ny - 1 + P are
 // only read by rows outside the grid and are zero-filled (no load beyond the guard).
-template <int P, int NC, int KK, int TYW, int R>
-__global__ void __launch_bounds__(32 * TYW, 2) k_spmv_rt(SpmvArgs a, int ntx, int nty) {
+template <int P, int NC, int KK, int TYW, int R, int MINB = 2, bool DB = true>
+__global__ void __launch_bounds__(32 * TYW, MINB) k_spmv_rt(SpmvArgs a, int ntx, int nty) {
   constexpr int W = 2 * P + 1, TX = 32 + 2 * P, TYR = TYW * R, TY = TYR + 2 * P, V = NC * KK;
   constexpr int PLANE = TY * TX * V;
   constexpr int NT = 32 * TYW;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(32 * TYW, 2) k_spmv_rt(SpmvArgs a, int ntx, in
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.st->launches, 1ull);
   extern __shared__ __align__(16) double smem_rt[];
   double* buf0 = smem_rt;
-  double* buf1 = smem_rt + PLANE;
+  double* buf1 = DB ? smem_rt + PLANE : smem_rt;
   const GridDesc g = a.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tx = blockIdx.x % ntx;
@@ -239,12 +239,15 @@ __global__ void __launch_bounds__(32 * TYW, 2) k_spmv_rt(SpmvArgs a, int ntx, in
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[r][v] = 0.0;
-  issue_plane(-P, buf0);
+  if (DB) issue_plane(-P, buf0);
 #pragma unroll 1
   for (int o3i = 0; o3i < W; ++o3i) {
     double* cur = (o3i & 1) ? buf1 : buf0;
     double* nxt = (o3i & 1) ? buf0 : buf1;
-    if (o3i + 1 < W) {
+    if (!DB) {  // single buffer: the other CTAs on the SM overlap this one's staging
+      issue_plane(o3i - P, cur);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else if (o3i + 1 < W) {
       issue_plane(o3i + 1 - P, nxt);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
@@ -398,10 +401,10 @@ static bool launch_tile(const SpmvArgs& a, cudaStream_t s) {
   return true;
 }
 
-template <int P, int NC, int KK, int TYW, int R>
+template <int P, int NC, int KK, int TYW, int R, int MINB = 2, bool DB = true>
 static bool launch_rt(const SpmvArgs& a, cudaStream_t s) {
   constexpr int TX = 32 + 2 * P, TY = TYW * R + 2 * P;
-  constexpr size_t bytes = sizeof(double) * 2 * TY * TX * NC * KK;
+  constexpr size_t bytes = sizeof(double) * (DB ? 2 : 1) * TY * TX * NC * KK;
   if constexpr (bytes > 200 * 1024) {
     return false;
   } else {
@@ -409,14 +412,14 @@ static bool launch_rt(const SpmvArgs& a, cudaStream_t s) {
     if (a.g.dim != 3 || a.g.nx < 32 || a.g.ny < TYW * R) return false;
     static bool attr = false;
     if (!attr) {
-      if (cudaFuncSetAttribute(k_spmv_rt<P, NC, KK, TYW, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if (cudaFuncSetAttribute(k_spmv_rt<P, NC, KK, TYW, R, MINB, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)bytes) != cudaSuccess)
         return false;
       attr = true;
     }
     const int ntx = (a.g.nx + 31) / 32, nty = (a.g.ny + TYW * R - 1) / (TYW * R);
     const unsigned int nb = (unsigned int)((long long)ntx * nty * a.g.nz);
-    k_spmv_rt<P, NC, KK, TYW, R><<<nb, 32 * TYW, bytes, s>>>(a, ntx, nty);
+    k_spmv_rt<P, NC, KK, TYW, R, MINB, DB><<<nb, 32 * TYW, bytes, s>>>(a, ntx, nty);
     if (a.mode == SPMV_PQ || a.mode == SPMV_TRUERES) k_spmv_fin<KK><<<1, 1024, 0, s>>>(a, nb);
     return true;
   }
@@ -455,6 +458,8 @@ static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
       if constexpr (NC == 3) {
         if (rt == 1 && launch_rt<P, NC, KK, 4, 4>(a, s)) return;  // 4 warps x 4 rows, 2 CTAs / SM
         if (rt == 2 && launch_rt<P, NC, KK, 8, 2>(a, s)) return;  // 8 warps x 2 rows, 2 CTAs / SM
+        // measured and dropped: single-buffered planes at 3 / 4 CTAs per SM (168 / 128 registers):
+        // 1.21 / 1.26 ms vs 1.22 ms, occupancy does not move it
       }
       if (g3 == 0 && a.g.dim == 3 && launch_tile<P, NC, KK>(a, s)) return;
       if (g3 == 4) launch_sm<P, NC, KK, false, 4>(a, (unsigned int)((nrb + 3) / 4), s);

@@ -1,7 +1,7 @@
 """GPU parity of the elastic mass SpMV (M = density * scalar M per component) on
 grids where the register-blocked row-tile kernel runs (k_spmv_rt: nx >= 32, ny >= 16, 3D;
 DESIGN.md "Elastic mass SpMV"): full and ragged x / y tiles, one right-hand side (ga_apply) and
-the k = 2 lock-stepped right-hand sides of the step's PCG, and sampled rows at C4's full size.
+the k = 1..4 lock-stepped right-hand sides of the step's PCG, and sampled rows at C4's full size.
 
 The oracle side is the scalar M of the same control net (oracle.assembly), applied per component;
 the elastic K of the step relation comes from the library's own K apply, which the small-grid
@@ -34,14 +34,25 @@ def _taylor(c, m, dt):
     return out
 
 
-@pytest.mark.parametrize("n", [32, 34], ids=["full_tiles", "ragged_tiles"])
-def test_elastic_mass_rowtiles_vs_oracle(n):
-    p = 2
-    cfg, prob, ctx, torch = _setup(p, n)
+_MCACHE = {}
+
+
+def _oracle_mass(prob, p, n):
     # scalar oracle M on the same (single-patch) control net: free DoFs in co-lexicographic
     # order = library order per component
-    d = assembly.Discretization(prob["patches"], p, n, 3)
-    M = d.M.tocsr()
+    if n not in _MCACHE:
+        _MCACHE[n] = assembly.Discretization(prob["patches"], p, n, 3).M.tocsr()
+    return _MCACHE[n]
+
+
+# k = number of lock-stepped right-hand sides of the PCG (KK template of the kernel: even KK
+# stages 16-byte pairs, odd KK single doubles)
+@pytest.mark.parametrize("n,k", [(32, 2), (34, 2), (34, 1), (34, 3), (34, 4)],
+                         ids=["full_tiles_k2", "ragged_k2", "ragged_k1", "ragged_k3", "ragged_k4"])
+def test_elastic_mass_rowtiles_vs_oracle(n, k):
+    p = 2
+    cfg, prob, ctx, torch = _setup(p, n, k=k)
+    M = _oracle_mass(prob, p, n)
     N = M.shape[0]
     rng = np.random.default_rng(21)
     x = rng.standard_normal(3 * N)
@@ -50,9 +61,8 @@ def test_elastic_mass_rowtiles_vs_oracle(n):
         ref = M @ x[c * N:(c + 1) * N]
         scale = abs(M).max() * np.abs(x).max()
         assert np.abs(y[c * N:(c + 1) * N] - ref).max() <= 1e-13 * scale, c
-    # one step, k = 2: both lock-stepped mass solves (KK = 2 row tiles inside the PCG) solve
+    # one step: the k lock-stepped mass solves (KK = k row tiles inside the PCG) solve
     # M y_j = -K s_j with the oracle's M (reading R1 for s_j)
-    k = cfg["k"]
     dt = 1e-3
     u0 = np.concatenate([prob["u0"][0][:, c].reshape((n + p,) * 3)[1:-1, 1:-1, 1:-1].reshape(-1) for c in range(3)])
     ctx.set_state(torch.tensor(u0, device="cuda"))
