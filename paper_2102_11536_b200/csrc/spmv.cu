@@ -465,6 +465,8 @@ static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
       if (g3 == 4) launch_sm<P, NC, KK, false, 4>(a, (unsigned int)((nrb + 3) / 4), s);
       else launch_sm<P, NC, KK, false, 8>(a, (unsigned int)((nrb + 7) / 8), s);
     } else {
+      // row tiles measured no faster for the scalar stencil (C3 p=2 n=96 k=1/3, p=2 n=192, p=4
+      // n=96: 0.81-0.95 vs 0.71-0.96 of HBM): one vector per row is not shared-memory bound
       launch_sm<P, NC, KK, false, 8>(a, (unsigned int)((nrb + 7) / 8), s);
     }
     return;
