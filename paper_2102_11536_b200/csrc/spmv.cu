@@ -457,7 +457,8 @@ static void spmv_kk(const SpmvArgs& a, cudaStream_t s) {
       if (rt < 0) { const char* e = getenv("GA_SPMV_RT"); rt = e ? atoi(e) : 1; }
       if constexpr (NC == 3) {
         if (rt == 1 && launch_rt<P, NC, KK, 4, 4>(a, s)) return;  // 4 warps x 4 rows, 2 CTAs / SM
-        if (rt == 2 && launch_rt<P, NC, KK, 8, 2>(a, s)) return;  // 8 warps x 2 rows, 2 CTAs / SM
+        // measured and dropped: 8 warps x 2 rows (1.33 vs 1.24 ms at C4); the x remainder
+        // (nx mod 32) as a second launch with narrow lane tiles (1.30 vs 1.22 ms: an extra wave)
         // measured and dropped: single-buffered planes at 3 / 4 CTAs per SM (168 / 128 registers):
         // 1.21 / 1.26 ms vs 1.22 ms, occupancy does not move it
       }

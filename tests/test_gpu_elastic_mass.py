@@ -47,8 +47,9 @@ def _oracle_mass(prob, p, n):
 
 # k = number of lock-stepped right-hand sides of the PCG (KK template of the kernel: even KK
 # stages 16-byte pairs, odd KK single doubles)
-@pytest.mark.parametrize("n,k", [(32, 2), (34, 2), (34, 1), (34, 3), (34, 4)],
-                         ids=["full_tiles_k2", "ragged_k2", "ragged_k1", "ragged_k3", "ragged_k4"])
+# free DoFs per direction n + p - 2: nx mod 32 = 0 (full x tiles), 2, 3, 6 (ragged last x tile)
+@pytest.mark.parametrize("n,k", [(32, 2), (34, 2), (34, 1), (34, 4), (35, 3), (38, 2)],
+                         ids=["full_tiles_k2", "rag2_k2", "rag2_k1", "rag2_k4", "rag3_k3", "rag6_k2"])
 def test_elastic_mass_rowtiles_vs_oracle(n, k):
     p = 2
     cfg, prob, ctx, torch = _setup(p, n, k=k)
