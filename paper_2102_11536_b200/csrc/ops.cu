@@ -557,7 +557,10 @@ static bool tile_multi_launch(TileMulti m, cudaStream_t s) {
     ST = tot16 >= 148 ? 16 : 8;
   }
   static int min_st = -1;  // GA_TILE_MINST: smallest slots per tile (8: up to 16 warps per CTA)
-  if (min_st < 0) { const char* e = getenv("GA_TILE_MINST"); min_st = e ? atoi(e) : 8; }
+  if (min_st < 0) {  // clamped to 1..8: larger minimums would exceed 16 warps (512 threads) per CTA
+    const char* e = getenv("GA_TILE_MINST");
+    min_st = std::min(8, std::max(1, e ? atoi(e) : 8));
+  }
   while (ST > min_st && (C + 32 / ST - 1) / (32 / ST) > 16) ST >>= 1;
   if (min_st < 8) while (ST > min_st && (C + 32 / ST - 1) / (32 / ST) > 8) ST >>= 1;
   int t0 = 0;
