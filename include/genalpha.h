@@ -5,11 +5,14 @@
  *
  * Citations are PAPER.md line numbers (P:line) and DESIGN.md readings (Rn).
  *
- * Problem:  M U'' + K U = 0, U(0) = U0, U'(0) = V0, with M, K the
- * Galerkin mass and stiffness matrices of a maximal-regularity B-spline space
- * of degree p on one patch or on a conforming multi-patch domain,
- * homogeneous Dirichlet data on the whole boundary.  Damping and
- * forcing are zero (C = 0, F = 0).  Time stepping is the explicit order-2k
+ * Problem:  M U'' + C U' + K U = F, U(0) = U0, U'(0) = V0, with M, K
+ * the Galerkin mass and stiffness matrices of a maximal-regularity B-spline
+ * space of degree p on one patch or on a block-structured conforming
+ * multi-patch domain, Dirichlet data on the whole boundary:
+ * homogeneous by default, non-homogeneous by lifting (ga_set_dirichlet).
+ * C = 0 and F = 0 unless set: Rayleigh damping C = damp_a0 M + damp_a1 K
+ * (ga_desc, reading R16) and forcing F = G h(t) (ga_set_forcing, reading
+ * R15).  Time stepping is the explicit order-2k
  * scheme of P:398-431 (k mass solves + updates of the other 2k variables per
  * step), with the K-term reading R1 and parameter set R2 of DESIGN.md.  Each
  * mass solve is PCG with the diagonal-scaled Kronecker preconditioner
@@ -70,9 +73,14 @@ typedef struct {
   int dim;              /* 2 or 3                                                     */
   int ncomp;            /* 1: scalar wave u'' = div(omega^2 grad u);            */
                         /* dim: linear elasticity (lame_lambda, lame_mu, density)      */
-  int p;                /* spline degree, 1..8, maximal regularity C^{p-1}    */
+  int p;                /* spline degree, 1..7, maximal regularity C^{p-1}    */
   int n;                /* elements per direction per patch, >= 1                     */
-  int npatch;           /* >= 1                                                       */
+  int npatch;           /* 1..16.  Layouts are block-structured (each patch one cell   */
+                        /* of a coarse patch grid, identity orientation), so there is  */
+                        /* no interface list and no preconditioner choice in the       */
+                        /* descriptor: interfaces follow from the cells, and the       */
+                        /* preconditioner is always the banded Kronecker one (K4; the  */
+                        /* fast-diagonalisation variant K4' is not built)              */
   const ga_patch* patches;
   double omega;         /* wave speed (scalar wave)                                   */
   double lame_lambda, lame_mu, density; /* elasticity only                            */
@@ -89,7 +97,9 @@ typedef struct {
                         /*    ||r|| <= min(pcg_rtol ||b||, pcg_refine_rtol ||b - M x0||)*/
                         /*    (x0 = main-phase result; reaching pcg_maxit here is not   */
                         /*    an error).  1e-3 recommended for p >= 5 (kappa(M) ~1e8)   */
-  double unstable_factor; /* GA_ERR_UNSTABLE threshold on ||U||/||U_0||; 0 disables   */
+  double unstable_factor; /* GA_ERR_UNSTABLE threshold on ||U|| / sqrt(ref); ref =      */
+                        /* ||U0||^2 + dt^2 ||V0||^2, or the first non-zero ||U_n||^2  */
+                        /* of a run that starts from rest; 0 disables                 */
   int op_mode;          /* operator representation: */
                         /* 1: assembled column-index-free stencils (2p+1)^dim per row;  */
                         /* 2: matrix-free sum factorisation from the Gauss-point data   */
@@ -105,6 +115,7 @@ typedef struct {
 
 typedef struct {
   long long steps;          /* steps completed since the last ga_set_state/ga_set_chain */
+                            /* (statistics counter)                                     */
   long long solves;         /* mass solves completed                                    */
   long long pcg_iters[4];   /* total PCG iterations per block (incl. refinement)        */
   int last_iters[4];        /* iterations of the most recent solve, per block          */
@@ -116,6 +127,9 @@ typedef struct {
   long long kernel_launches;/* kernels of this library executed on the device since    */
                             /* the last ga_set_state (counted on the device)            */
   long long loop_iters;     /* lock-stepped PCG iterations executed (all solves)        */
+  long long step_index;     /* simulation step n of the state (t_n = t0 + n dt for the   */
+                            /* forcing): 0 after ga_set_state, +1 per step, NOT reset by */
+                            /* ga_set_chain, set by ga_set_time                         */
 } ga_stats;
 
 /* Generalized-alpha parameters of the k blocks (host only, no GPU).
@@ -170,6 +184,11 @@ ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void
 ga_status ga_set_forcing(ga_ctx* ctx, const double* d_G, int nterms, const double* amp, const double* omega,
                          const double* phase, double t0, void* stream);
 
+/* Set the simulation step index n (t_n = t0 + n dt of the forcing and lifting time functions),
+ * e.g. after restoring a checkpoint into a fresh context with ga_set_chain.  Asynchronous.
+ * GA_ERR_ARG if step_index < 0. */
+ga_status ga_set_time(ga_ctx* ctx, long long step_index, void* stream);
+
 /* Non-homogeneous Dirichlet data by lifting, single patch,
  * scalar wave: the boundary control coefficients are U_b(t) = g_b h_D(t), h_D(t) = sum_{i<nterms}
  * amp_i cos(omega_i t + phase_i), 1 <= nterms <= 4.  h_g: HOST array of all (n+p)^dim control
@@ -191,7 +210,9 @@ ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream);
 /* Copy U, V, A (c0, c1, c2) to caller vectors; any pointer may be NULL. */
 ga_status ga_get_state(ga_ctx* ctx, double* d_u, double* d_v, double* d_a, void* stream);
 
-/* Checkpoint / resume of the whole chain c_m, m = 0..3k-1 (free-DoF vectors). */
+/* Checkpoint / resume of the whole chain c_m, m = 0..3k-1 (free-DoF vectors).  ga_set_chain
+ * with m = 0 resets the statistics and the failure status but keeps the simulation step index
+ * (ga_stats.step_index; set it with ga_set_time when resuming in a new context). */
 ga_status ga_get_chain(ga_ctx* ctx, int m, double* d_out, void* stream);
 ga_status ga_set_chain(ga_ctx* ctx, int m, const double* d_in, void* stream);
 
@@ -210,7 +231,9 @@ ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters,
 /* lambda_max(M^{-1} K) by `iters` (<= 512) Lanczos steps in the M inner product (each one K
  * apply, one PCG mass solve and one M apply; no reorthogonalisation: the extremal Ritz value
  * converges first), for the CFL time step dt = c sqrt(theta_max / lambda_max).  The time-
- * stepping state is left unchanged.  SYNCHRONIZES stream. */
+ * stepping state (chain, predictors, forcing slots) and the statistics / status are restored
+ * on every return path, so a Lanczos solve never counts as a step solve and a Lanczos NOCONV
+ * is returned, not latched.  SYNCHRONIZES stream. */
 ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream);
 
 /* host_map[f] = patch * (n+p)^dim + local control-point index (co-lex) of
@@ -225,6 +248,8 @@ ga_status ga_free_dof_map(const ga_ctx* ctx, long long* host_map);
  *     (scaling + all line sweeps + r.z/r.r reductions), 3 = predictor pass of
  *     the stage kernel (reads the 3k chain, writes the k predictors),
  *     4 = M stencil SpMV without reduction, 5 = PCG direction update p = z + beta p,
+ *     (ops 2 and 5 run on a profiling PcgState with every block active and beta != 0, so
+ *     they do their full work; the PcgState is zeroed afterwards),
  *     6 = one complete lock-stepped mass solve of the current right-hand sides
  *     (the persistent solver kernel on small grids; its step graph otherwise). */
 /* Persistent-solver mode: 1 if ga_create chose the single-kernel cooperative PCG

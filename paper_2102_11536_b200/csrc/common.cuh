@@ -40,7 +40,10 @@ struct DevStatus {
   int last_iters[KMAX];
   int max_iters;
   double max_relres;
-  double u0norm2;             // ||U_0||^2 for the instability detector
+  double u0norm2;             // instability reference: ||U_0||^2 + dt^2 ||V_0||^2, or the first
+                              // non-zero ||U_n||^2 when the run starts from rest (0 = not yet set)
+  long long tstep;            // simulation step index n (t_n = t0 + n dt of the forcing); reset by
+                              // ga_set_state / ga_set_time only, never by ga_set_chain
   unsigned long long launches;
   long long loop_iters;       // lock-stepped PCG iterations executed
 };

@@ -1113,14 +1113,19 @@ __global__ void k_lz_norm(GridDesc g, int nvec, int kk, double* v, const double*
 }
 __global__ void k_lz_copy_alpha(const double* src, double* dst) { dst[0] = -src[0]; }
 
-__global__ void k_reset_status(DevStatus* st, PcgState* pc) {
+__global__ void k_reset_status(DevStatus* st, PcgState* pc, int keep_time) {
+  const long long tstep = keep_time ? st->tstep : 0;
   memset(st, 0, sizeof(DevStatus));
+  st->tstep = tstep;
   st->fail_step = -1;
   st->fail_block = -1;
   memset(pc, 0, sizeof(PcgState));
 }
 
-static void reset_status(ga_ctx* ctx, cudaStream_t s) { k_reset_status<<<1, 1, 0, s>>>(ctx->st, ctx->pcg); }
+// keep_time: the simulation step index (forcing clock) survives, e.g. ga_set_chain on a resume
+static void reset_status(ga_ctx* ctx, cudaStream_t s, int keep_time = 0) {
+  k_reset_status<<<1, 1, 0, s>>>(ctx->st, ctx->pcg, keep_time);
+}
 
 static ga_status check_ctx(ga_ctx* ctx) {
   if (!ctx) { seterr(nullptr, "ctx is NULL"); return GA_ERR_ARG; }
@@ -1143,8 +1148,11 @@ static ga_status set_predictors_and_norm(ga_ctx* ctx, cudaStream_t s) {
     if (rc != GA_OK) return rc;
   }
   launch_predict(stage_args(ctx), s);
-  // ||U0||^2 for the instability detector
-  launch_dot(ctx->g, ctx->nvec, 1, ctx->chain, ctx->chain, &ctx->st->u0norm2, ctx->partial, ctx->counter, s);
+  // reference of the instability detector: ||U0||^2 + dt^2 ||V0||^2 (0 from rest: the first
+  // non-zero ||U_n||^2 is adopted by the stage kernel)
+  const long long vstride = (long long)ctx->nvec * ctx->g.padded;
+  launch_ref_norm(ctx->g, ctx->nvec, ctx->chain, ctx->chain + vstride, ctx->d.dt, ctx->st, ctx->partial,
+                  ctx->counter, s);
   CK(cudaGetLastError());
   return GA_OK;
 }
@@ -1316,11 +1324,22 @@ ga_status ga_set_chain(ga_ctx* ctx, int m, const double* d_in, void* stream) {
   if (m < 0 || m >= 3 * ctx->k || !d_in) { seterr(ctx, "bad chain index or NULL"); return GA_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   const long long vstride = (long long)ctx->nvec * ctx->g.padded;
-  if (m == 0) reset_status(ctx, s);
+  if (m == 0) reset_status(ctx, s, /*keep_time=*/1);  // the forcing clock is not the statistics
   launch_api_to_grid(ctx->g, ctx->nvec, ctx->nfree, ctx->map, d_in, ctx->chain + m * vstride, 1, 0, ctx->st, s);
   CK(cudaGetLastError());
   // predictors and ||U0|| follow the chain; cheap to refresh after every entry
   return set_predictors_and_norm(ctx, s);
+}
+
+__global__ void k_set_tstep(DevStatus* st, long long n) { st->tstep = n; }
+
+ga_status ga_set_time(ga_ctx* ctx, long long step_index, void* stream) {
+  ga_status rc = check_ctx(ctx);
+  if (rc != GA_OK) return rc;
+  if (step_index < 0) { seterr(ctx, "step_index < 0"); return GA_ERR_ARG; }
+  k_set_tstep<<<1, 1, 0, (cudaStream_t)stream>>>(ctx->st, step_index);
+  CK(cudaGetLastError());
+  return GA_OK;
 }
 
 ga_status ga_get_state(ga_ctx* ctx, double* d_u, double* d_v, double* d_a, void* stream) {
@@ -1354,6 +1373,7 @@ ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream) {
   out->fail_block = h.fail_block;
   out->kernel_launches = (long long)h.launches;
   out->loop_iters = h.loop_iters;
+  out->step_index = h.tstep;
   return GA_OK;
 }
 
@@ -1371,6 +1391,19 @@ ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
     return GA_OK;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  if (op == 2 || op == 5) {
+    // a profiling PcgState in which every block is active, past its first iteration and with
+    // beta != 0, so the direction update and the preconditioner do their full work (the state
+    // left by the last solve has every block converged: those kernels would return at once)
+    PcgState h;
+    memset(&h, 0, sizeof(h));
+    for (int j = 0; j < KMAX; ++j) {
+      h.active[j] = j < ctx->k ? 1 : 0;
+      h.alpha[j] = 0.5; h.beta[j] = 0.25; h.rz[j] = h.rzold[j] = h.bb[j] = 1.0;
+    }
+    h.nrhs = ctx->k; h.iter = 1; h.pfirst = 0; h.first = 0;
+    CK(cudaMemcpyAsync(ctx->pcg, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  }
   for (int i = 0; i < reps; ++i) {
     switch (op) {
       case 0: launch_spmv(spmv_args(ctx, 0, ctx->pv, ctx->q, SPMV_PQ), s); break;
@@ -1386,6 +1419,7 @@ ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
       default: launch_p_update(vec_args(ctx), s); break;
     }
   }
+  if (op == 2 || op == 5) CK(cudaMemsetAsync(ctx->pcg, 0, sizeof(PcgState), s));
   CK(cudaGetLastError());
   return GA_OK;
 }
@@ -1455,19 +1489,36 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
   // the predictor MV is state: keep a host copy and restore it at the end
   std::vector<double> hsave(mvbytes / sizeof(double));
   CK(cudaMemcpyAsync(hsave.data(), ctx->pred, mvbytes, cudaMemcpyDeviceToHost, s));
+  // the statistics and the failure status are state too: the Lanczos solves must not count as
+  // step solves, and a NOCONV inside Lanczos is returned, not latched (restored on every exit)
+  DevStatus stsave;
+  CK(cudaMemcpyAsync(&stsave, ctx->st, sizeof(stsave), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  auto restore = [&](ga_status rc0) -> ga_status {
+    cudaError_t e1 = cudaMemcpyAsync(ctx->pred, hsave.data(), mvbytes, cudaMemcpyHostToDevice, s);
+    cudaError_t e2 = cudaMemcpyAsync(ctx->st, &stsave, sizeof(stsave), cudaMemcpyHostToDevice, s);
+    cudaError_t e3 = cudaStreamSynchronize(s);
+    ga_status rs = set_step_slots(ctx, s);
+    if (rc0 != GA_OK) return rc0;
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      seterr(ctx, "ga_lambda_max: restoring the state failed");
+      return GA_ERR_CUDA;
+    }
+    return rs;
+  };
   if (ctx->forcing) {  // the K-solve graph would add F: switch the slots off meanwhile
     ForceSlots fs;
     memset(&fs, 0, sizeof(fs));
-    CK(cudaMemcpyAsync(ctx->fslots, &fs, sizeof(fs), cudaMemcpyHostToDevice, s));
+    if ((cudaMemcpyAsync(ctx->fslots, &fs, sizeof(fs), cudaMemcpyHostToDevice, s)) != cudaSuccess) return restore(GA_ERR_CUDA);
   }
-  CK(cudaStreamSynchronize(s));
+  if ((cudaStreamSynchronize(s)) != cudaSuccess) return restore(GA_ERR_CUDA);
   double* vp = ctx->lzv;                                   // v_{j-1} (then w)
   double* vc = ctx->lzv + (size_t)nvec * g.padded * k;     // v_j
   double* al = ctx->lzab;                                  // alpha_j, j < iters
   double* be = ctx->lzab + LZMAX + 2;                      // beta_j (be[0] = norm of the start vector)
   double* dn = ctx->dscal;
-  CK(cudaMemsetAsync(ctx->lzv, 0, 2 * mvbytes, s));
-  CK(cudaMemsetAsync(ctx->lzab, 0, sizeof(double) * 2 * (LZMAX + 2), s));
+  if ((cudaMemsetAsync(ctx->lzv, 0, 2 * mvbytes, s)) != cudaSuccess) return restore(GA_ERR_CUDA);
+  if ((cudaMemsetAsync(ctx->lzab, 0, sizeof(double) * 2 * (LZMAX + 2), s)) != cudaSuccess) return restore(GA_ERR_CUDA);
   k_altsign<<<nb, 256, 0, s>>>(g, nvec, k, vc, ctx->mask);
   // v_1 = v / ||v||_M
   launch_spmv(spmv_args(ctx, 0, vc, ctx->q, SPMV_APPLY), s);
@@ -1475,11 +1526,11 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
   k_lz_norm<<<nb, 256, 0, s>>>(g, nvec, k, vc, dn, be);
   int done = iters;
   for (int j = 0; j < iters; ++j) {
-    CK(cudaMemsetAsync(ctx->pred, 0, mvbytes, s));
-    CK(cudaMemcpy2DAsync(ctx->pred, sizeof(double) * k, vc, sizeof(double) * k, sizeof(double),
-                         (size_t)nvec * g.padded, cudaMemcpyDeviceToDevice, s));
+    if ((cudaMemsetAsync(ctx->pred, 0, mvbytes, s)) != cudaSuccess) return restore(GA_ERR_CUDA);
+    if ((cudaMemcpy2DAsync(ctx->pred, sizeof(double) * k, vc, sizeof(double) * k, sizeof(double),
+                         (size_t)nvec * g.padded, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return restore(GA_ERR_CUDA);
     rc = run_kind(ctx, GK_SOLVEK, s);  // b = -K v_j, x = M^{-1} b
-    if (rc != GA_OK) return rc;
+    if (rc != GA_OK) return restore(rc);
     launch_dot(g, nvec, k, vc, ctx->b, dn, ctx->partial, ctx->counter, s);  // -alpha_j
     k_lz_copy_alpha<<<1, 1, 0, s>>>(dn, al + j);
     // w = A v_j - alpha_j v_j - beta_{j-1} v_{j-1}, into vp
@@ -1488,18 +1539,17 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
     launch_dot(g, nvec, k, vp, ctx->q, dn + 1, ctx->partial, ctx->counter, s);
     k_lz_norm<<<nb, 256, 0, s>>>(g, nvec, k, vp, dn + 1, be + j + 1);
     std::swap(vp, vc);  // v_{j+1} = w / beta_j becomes current, v_j previous
-    CK(cudaGetLastError());
+    if (cudaGetLastError() != cudaSuccess) return restore(GA_ERR_CUDA);
   }
   std::vector<double> ha(done), hb(done + 1);
-  CK(cudaMemcpyAsync(ha.data(), al, sizeof(double) * done, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hb.data(), be, sizeof(double) * (done + 1), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(ctx->pred, hsave.data(), mvbytes, cudaMemcpyHostToDevice, s));
   DevStatus hs;
-  CK(cudaMemcpyAsync(&hs, ctx->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  rc = set_step_slots(ctx, s);
+  if (cudaMemcpyAsync(ha.data(), al, sizeof(double) * done, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(hb.data(), be, sizeof(double) * (done + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(&hs, ctx->st, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return restore(GA_ERR_CUDA);
+  rc = restore(hs.status != 0 ? (ga_status)hs.status : GA_OK);
   if (rc != GA_OK) return rc;
-  if (hs.status != 0) return (ga_status)hs.status;
   // stop at a (numerically) invariant subspace: beta_j ~ 0
   int m = done;
   for (int j = 1; j < done; ++j)

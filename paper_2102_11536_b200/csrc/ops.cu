@@ -1034,7 +1034,11 @@ __global__ void __launch_bounds__(NTHREADS) k_stage(StageArgs a) {
   if (reduce_last_block<1>(u2, a.partial, a.counter, out)) {
     DevStatus* st = a.st;
     st->steps += 1;
-    if (a.unstable2 > 0.0 && !(out[0] <= a.unstable2 * st->u0norm2)) {
+    st->tstep += 1;
+    // reference of the instability detector: set at ga_set_state from U0 and dt V0; a run that
+    // starts from rest (U0 = V0 = 0: forcing or lifting) adopts its first non-zero ||U_n||^2
+    if (st->u0norm2 == 0.0) st->u0norm2 = out[0];
+    else if (a.unstable2 > 0.0 && !(out[0] <= a.unstable2 * st->u0norm2)) {
       st->status = -6;  // GA_ERR_UNSTABLE
       st->fail_step = st->steps;
       st->fail_block = -1;
@@ -1049,7 +1053,7 @@ __global__ void __launch_bounds__(NTHREADS) k_add_forcing(ForceArgs a) {
   const GridDesc g = a.g;
   // h_r^{(m)}(t) per pair and slot, identical in every thread (a few terms, computed redundantly)
   double hj[FMAXPAIRS][KK];
-  const double tn = a.t0 + (double)a.st->steps * a.dt;
+  const double tn = a.t0 + (double)a.st->tstep * a.dt;
 #pragma unroll
   for (int r = 0; r < FMAXPAIRS; ++r)
 #pragma unroll
@@ -1209,6 +1213,28 @@ __global__ void __launch_bounds__(NTHREADS) k_dot(GridDesc g, int nvec, int kk, 
   }
   double out[1];
   if (reduce_last_block<1>(v, partial, counter, out)) *outp = out[0];
+}
+// reference norm of the instability detector: ||c0||^2 + tau^2 ||c1||^2 (slot 0 of the chain)
+__global__ void __launch_bounds__(NTHREADS) k_ref_norm(GridDesc g, int nvec, const double* c0, const double* c1,
+                                                       double tau, DevStatus* st, double* partial,
+                                                       unsigned int* counter) {
+  const long long tot = (long long)nvec * g.npts;
+  const long long estride = (long long)gridDim.x * blockDim.x;
+  double v[1] = {0.0};
+  for (long long e = (long long)gtid(); e < tot; e += estride) {
+    const long long i = e % g.npts;
+    const int c = (int)(e / g.npts);
+    const long long idx = (long long)c * g.padded + g.guard + i;
+    const double w = tau * c1[idx];
+    v[0] = fma(c0[idx], c0[idx], fma(w, w, v[0]));
+  }
+  double out[1];
+  if (reduce_last_block<1>(v, partial, counter, out)) st->u0norm2 = out[0];
+}
+void launch_ref_norm(const GridDesc& g, int nvec, const double* c0, const double* c1, double tau, DevStatus* st,
+                     double* partial, unsigned int* counter, cudaStream_t s) {
+  const long long tot = (long long)nvec * g.npts;
+  k_ref_norm<<<red_grid(tot), NTHREADS, 0, s>>>(g, nvec, c0, c1, tau, st, partial, counter);
 }
 void launch_dot(const GridDesc& g, int nvec, int kk, const double* a, const double* b, double* out, double* partial,
                 unsigned int* counter, cudaStream_t s) {

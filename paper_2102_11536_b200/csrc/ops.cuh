@@ -163,6 +163,8 @@ void launch_grid_to_api(const GridDesc& g, int nvec, long long nfree, const long
                         int kk, int slot, double* api, DevStatus* st, cudaStream_t s);
 
 // dot products of MV slot 0 of two grid vectors (stride kk) into out[0] (device), via partials.
+void launch_ref_norm(const GridDesc& g, int nvec, const double* c0, const double* c1, double tau, DevStatus* st,
+                     double* partial, unsigned int* counter, cudaStream_t s);
 void launch_dot(const GridDesc& g, int nvec, int kk, const double* a, const double* b, double* out,
                 double* partial, unsigned int* counter, cudaStream_t s);
 void launch_scale(const GridDesc& g, int nvec, int kk, double* a, const double* num, int inv_sqrt,

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
                 -4: "GA_ERR_CONFORMITY", -5: "GA_ERR_NOCONV", -6: "GA_ERR_UNSTABLE",
                 -7: "GA_ERR_CUDA", -8: "GA_ERR_OOM"}
 
-EXPORTED = ["ga_params", "ga_spectral_scan", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_set_dirichlet", "ga_advance", "ga_get_state",
+EXPORTED = ["ga_params", "ga_spectral_scan", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_set_time", "ga_set_dirichlet", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
             "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_operator_mode", "ga_destroy",
             "ga_last_error"]
@@ -46,7 +46,7 @@ class ga_stats(ctypes.Structure):
     _fields_ = [("steps", c_longlong), ("solves", c_longlong), ("pcg_iters", c_longlong * 4),
                 ("last_iters", c_int * 4), ("max_iters", c_int), ("max_rel_residual", c_double),
                 ("status", c_int), ("fail_step", c_longlong), ("fail_block", c_int),
-                ("kernel_launches", c_longlong), ("loop_iters", c_longlong)]
+                ("kernel_launches", c_longlong), ("loop_iters", c_longlong), ("step_index", c_longlong)]
 
 
 class GAError(RuntimeError):
@@ -69,6 +69,7 @@ def _load():
         "ga_set_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
         "ga_advance": (c_int, [c_void_p, c_int, c_void_p]),
         "ga_set_forcing": (c_int, [c_void_p, c_void_p, c_int, P, P, P, c_double, c_void_p]),
+        "ga_set_time": (c_int, [c_void_p, c_longlong, c_void_p]),
         "ga_set_dirichlet": (c_int, [c_void_p, P, c_int, P, P, P, c_void_p, c_size_t, c_void_p]),
         "ga_get_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
         "ga_get_chain": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
@@ -220,6 +221,11 @@ class Context:
         _check(lib.ga_set_dirichlet(self.ctx, gp, n, arr[0], arr[1], arr[2], _aligned(scratch), sc, self._s()),
                self.ctx)
         del scratch
+
+    def set_time(self, step_index):
+        """Simulation step index n of the state (t_n = t0 + n dt of the forcing), e.g. after
+        ga_set_chain into a fresh context."""
+        _check(lib.ga_set_time(self.ctx, int(step_index), self._s()), self.ctx)
 
     def advance(self, nsteps):
         _check(lib.ga_advance(self.ctx, int(nsteps), self._s()), self.ctx)
