@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "assembly.cuh"
+#include "common.cuh"
 
 namespace ga {
 
@@ -240,6 +241,10 @@ __global__ void k_contract_final(const double* __restrict__ in, const double* __
   if (f.half) {  // o >= 0 only (index o - S/2), rows shifted by the zero guard
     const long long Sh = (f.S + 1) / 2, hl = olin - f.S / 2;
     if (hl < 0) return;
+    if (f.sym) {
+      coef[sym_index(gr[0], gr[1], DIM == 3 ? gr[2] : 0, hl, f.sxs, f.snseg, f.G[1], Sh)] += s;
+      return;
+    }
     const long long rr = grow + f.hguard;
     coef[((rr >> 5) * Sh + hl) * 32 + (rr & 31)] += s;
     return;

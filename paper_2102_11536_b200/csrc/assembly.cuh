@@ -36,6 +36,7 @@ struct FinalDesc {
   const unsigned char* mask;
   int half;                    // half-symmetric layout: offsets o >= 0 only, rows shifted by hguard
   long long hguard;
+  int sym, sxs, snseg;         // 3D scalar half layout: segment-blocked (common.cuh sym_index)
   // boundary apply (Dirichlet lifting): instead of storing coefficients, accumulate
   // bout[row] += A(row, col) bg[col] over the boundary columns col (patch-local full index)
   const double* bg;

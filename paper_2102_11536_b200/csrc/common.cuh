@@ -64,6 +64,28 @@ struct GridDesc {
   long long cs;               // row stride of the stencil coefficient arrays (npts rounded up to 32)
 };
 
+// Segment-blocked layout of the 3D half-symmetric stencils (spmv_sym.cu): each x-line of nx
+// points is split into nseg = ceil(nx / 32) segments of XS = 32 points (the last one partial).
+// Row block b = seg + nseg (y + ny z); coefficient h (0 <= h < Sh) of point x = 32 seg + l at
+// ((b Sh + h) 32 + l): one offset of a block is 256 contiguous bytes, so a warp load is whole
+// 64-byte DRAM granules and every offset of the kernel's loads is an immediate.
+constexpr int SYM_STRIDE = 32;
+struct SymLayout {
+  int xs, nseg;
+};
+inline SymLayout sym_layout(int nx) {
+  SymLayout L;
+  L.nseg = (nx + 31) / 32;
+  L.xs = SYM_STRIDE;
+  return L;
+}
+__host__ __device__ __forceinline__ long long sym_index(int x, int y, int z, long long h, int xs, int nseg, int ny,
+                                                        long long Sh) {
+  const int seg = x / xs;
+  const long long b = seg + (long long)nseg * (y + (long long)ny * z);
+  return (b * Sh + h) * SYM_STRIDE + (x - seg * xs);
+}
+
 __device__ __forceinline__ unsigned long long gtid() {
   return (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
 }

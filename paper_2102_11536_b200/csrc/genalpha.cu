@@ -78,6 +78,9 @@ struct ga_ctx {
   bool persist = false;  // small single-patch scalar problems: one cooperative kernel per solve
   bool mf = false;       // matrix-free M (and scalar K): sum factorisation from Gauss-point data
   bool half = false;     // half-symmetric stencils (offsets o >= 0, zero guard of g.guard rows)
+  bool sym = false;      // 3D scalar half stencils in the segment-blocked layout (spmv_sym.cu)
+  double* symzero = nullptr;  // zero block read by the single-read SpMV for unstored rows
+  SymLayout sl = {0, 0};
   double *mfWM = nullptr, *mfWK = nullptr, *mftv = nullptr, *mftd = nullptr, *diagM = nullptr;
   double *mpT1 = nullptr, *mpT2 = nullptr, *mpT3 = nullptr;  // 3D multi-pass mass intermediates
   // forcing F = G h(t) (ga_set_forcing): grid vector, device slot table, host parameters
@@ -110,7 +113,7 @@ void seterr(ga_ctx* ctx, const std::string& s) {
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t off_coefM, off_coefK, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
+  size_t off_coefM, off_coefK, off_symzero, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
       off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots,
       off_lz, off_lzab;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
@@ -130,6 +133,8 @@ struct Shape {
   int pmin[3], pmax[3];
   bool mf = false;     // matrix-free operators (op_mode 2, or auto)
   bool half = false;   // half-symmetric stencils (op_mode 3, or auto)
+  bool sym = false;    // ... in the segment-blocked layout of the single-read 3D SpMV (scalar, 3D)
+  SymLayout sl = {0, 0};
 };
 
 int op_auto(const ga_desc* d);
@@ -177,6 +182,7 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
     sh.mf = pick == 2;
     sh.half = pick == 3;
   }
+  sh.sym = sh.half && d->dim == 3 && d->ncomp == 1;
   sh.S = (long long)sh.W1 * sh.W1 * (sh.dim == 3 ? sh.W1 : 1);
   const int m = sh.m, dim = sh.dim;
   int cmax[3] = {0, 0, 0};
@@ -192,6 +198,7 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
   sh.g.guard = guard;
   sh.g.padded = sh.g.npts + 2 * guard;
   sh.g.cs = (sh.g.npts + 31) / 32 * 32;
+  sh.sl = sym_layout(sh.g.nx);
   // occupancy of coarse cells
   std::map<long long, int> cellid;
   auto ckey = [&](int x, int y, int z) { return ((long long)z * 1000 + y) * 1000 + x; };
@@ -308,6 +315,15 @@ int op_auto(const ga_desc* d) {
 
 constexpr int LZMAX = 512;  // Lanczos steps of ga_lambda_max
 
+// bytes of one scalar stencil operator (M, or the scalar K) in the layout of the shape
+size_t coef_bytes(const Shape& sh) {
+  const long long Sh = (sh.S + 1) / 2;
+  if (sh.sym)
+    return sizeof(double) * Sh * SYM_STRIDE * (long long)sh.sl.nseg * sh.g.ny * sh.g.nz;
+  if (sh.half) return sizeof(double) * Sh * ((sh.g.npts + sh.g.guard + 31) / 32 * 32);
+  return sizeof(double) * sh.S * sh.g.cs;
+}
+
 size_t sweep_bytes(int n, int p) {
   // dinv + coef + H + A (L <= 6 levels, C <= 64 chunks)
   return align256(sizeof(double) * ((size_t)n * (1 + 2 * p) + (size_t)6 * 64 * p * p));
@@ -319,10 +335,10 @@ Layout make_layout(const Shape& sh) {
   auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
   const long long npts = sh.g.npts;
   const bool mfK = sh.mf && sh.nvec == 1;  // the elastic K stays a full stencil
-  const long long Sh = (sh.S + 1) / 2, hrows = (npts + sh.g.guard + 31) / 32 * 32;
-  const size_t mbytes = sh.half ? sizeof(double) * Sh * hrows : sizeof(double) * sh.S * sh.g.cs;
+  const size_t mbytes = coef_bytes(sh);
   L.off_coefM = take(sh.mf ? 0 : mbytes);
   L.off_coefK = take(mfK ? 0 : (sh.nvec == 3 ? sizeof(double) * sh.S * sh.g.cs * 9 : mbytes));
+  L.off_symzero = take(sh.sym ? sizeof(double) * ((sh.S + 1) / 2) * SYM_STRIDE : 0);
   {
     const long long nq = (long long)sh.n * (sh.p + 1);
     const long long nqd = sh.dim == 3 ? nq * nq * nq : nq * nq;
@@ -392,7 +408,7 @@ size_t asm_fixed_bytes(const Shape& sh) {
 
 __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, int loz, const double* d0,
                           const double* d1, const double* d2, const double* coefM, const double* diagM, long long S,
-                          int nx, int ny, const unsigned char* mask, long long hguard) {
+                          int nx, int ny, const unsigned char* mask, long long hguard, SymLayout sl) {
   const long long nbox = (long long)bx * by * bz;
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nbox) return;
@@ -404,8 +420,9 @@ __global__ void k_scaling(double* s, int bx, int by, int bz, int lox, int loy, i
     // diag(M): matrix-free array, or the centre offset of the blocked stencil layout
     const long long hr = gi + hguard;  // half-symmetric layout: centre offset = index 0
     const double D = diagM ? diagM[gi]
-                           : (hguard >= 0 ? coefM[((hr >> 5) * ((S + 1) / 2)) * 32 + (hr & 31)]
-                                          : coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)]);
+                           : (sl.xs > 0 ? coefM[sym_index(lox + ix, loy + iy, loz + iz, 0, sl.xs, sl.nseg, ny, (S + 1) / 2)]
+                              : hguard >= 0 ? coefM[((hr >> 5) * ((S + 1) / 2)) * 32 + (hr & 31)]
+                                            : coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)]);
     v = sqrt(dh / D);  // s = sqrt(Dh / D): calM^{-1} = S Mh^{-1} S
   }
   s[e] = v;
@@ -458,6 +475,7 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
   if (c->half && !a.elastic) { a.half = 1; a.hguard = c->g.guard; }
+  if (c->sym && !a.elastic) { a.sym = 1; a.sxs = c->sl.xs; a.snseg = c->sl.nseg; a.symzero = c->symzero; }
   if (c->mf && !a.elastic) {
     a.mf = 1; a.mfstiff = which; a.mfn = c->n; a.mfj0 = 0;
     a.mfW = which == 0 ? c->mfWM : c->mfWK; a.mfws = c->mfws;
@@ -664,8 +682,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
   if (off > scratch_bytes) { seterr(ctx, "scratch too small (slab)"); return GA_ERR_OOM; }
 
   const bool mfK = sh.mf && sh.nvec == 1;
-  const long long Sh = (sh.S + 1) / 2, hrows = (sh.g.npts + sh.g.guard + 31) / 32 * 32;
-  const size_t mbytes = sh.half ? sizeof(double) * Sh * hrows : sizeof(double) * sh.S * sh.g.cs;
+  const size_t mbytes = coef_bytes(sh);
   if (!sh.mf && !bapply) CK(cudaMemsetAsync(ctx->coefM, 0, mbytes, s));
   if (!mfK && !bapply) CK(cudaMemsetAsync(ctx->coefK, 0, sh.nvec == 3 ? sizeof(double) * sh.S * sh.g.cs * 9 : mbytes, s));
   // term list: (target block pointer, spec, derivative flags per direction)
@@ -758,6 +775,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         f.mask = ctx->mask;
         f.half = (sh.half && f.ncf == 1) ? 1 : 0;  // the elastic K stays full
         f.hguard = sh.g.guard;
+        f.sym = sh.sym ? 1 : 0; f.sxs = sh.sl.xs; f.snseg = sh.sl.nseg;
         if (bapply) { f.bg = bg; f.bout = (t.coef == ctx->coefM) ? boutM : boutK; }
         if (dim == 3) {
           ContractDesc c2;
@@ -935,6 +953,9 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->coefK = (double*)(ws + L.off_coefK);
   ctx->mf = sh.mf;
   ctx->half = sh.half;
+  ctx->sym = sh.sym;
+  ctx->sl = sh.sl;
+  ctx->symzero = (double*)(ws + L.off_symzero);
   if (sh.mf) {
     const long long nq = (long long)sh.n * (sh.p + 1);
     ctx->mfws = sh.dim == 3 ? nq * nq * nq : nq * nq;
@@ -978,6 +999,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   // zero everything small + vectors (guards must be zero/finite)
   CKD(cudaMemsetAsync(ws + L.off_chain, 0, L.off_mask - L.off_chain, s));
   CKD(cudaMemsetAsync(ws + L.off_pcg, 0, L.off_dscal + 256 - L.off_pcg, s));
+  if (sh.sym) CKD(cudaMemsetAsync(ws + L.off_symzero, 0, sizeof(double) * ((sh.S + 1) / 2) * SYM_STRIDE, s));
   if (multi) {
     CKD(cudaMemcpyAsync(ctx->mask, sh.mask.data(), sh.g.npts, cudaMemcpyHostToDevice, s));
     CKD(cudaMemcpyAsync(ctx->map, sh.map.data(), sizeof(long long) * sh.nfree, cudaMemcpyHostToDevice, s));
@@ -1054,7 +1076,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
                                                                  pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
                                                                  center, ctx->diagM, ctx->S, sh.g.nx, sh.g.ny, ctx->mask,
-                                                                 sh.half ? sh.g.guard : -1);
+                                                                 sh.half ? sh.g.guard : -1,
+                                                                 sh.sym ? sh.sl : SymLayout{0, 0});
     CKD(cudaGetLastError());
     CKD(cudaStreamSynchronize(s));  // tmp reused by the next patch
   }

@@ -46,11 +46,16 @@ struct SpmvArgs {
   // hguard rows (spmv_core.cuh spmv_block_half); not for the elastic (3x3-block) K
   int half;
   long long hguard;
+  // 3D scalar half-symmetric operators in the segment-blocked layout of the single-read SpMV
+  // (sym = 1, spmv_sym.cu): XS points per x-segment, nseg segments per x-line
+  int sym, sxs, snseg;
+  const double* symzero;  // zero block of Sh x 32 doubles (loads of unstored / outside rows)
   // 3D matrix-free mass by the multi-pass non-redundant sum factorisation (matfree_mp.cu):
   // intermediates T1 [c][n_q][nf][nf][k], T2 / T3 [c][n_q][n_q][nf][k]
   double *mpT1, *mpT2, *mpT3;
 };
 void launch_spmv(const SpmvArgs& a, cudaStream_t s);
+void launch_spmv_sym(const SpmvArgs& a, cudaStream_t s);  // a.sym = 1 (spmv_sym.cu)
 // matrix-free variants (matfree.cu): the same contract as launch_spmv for a.mf = 1
 void launch_matfree(const SpmvArgs& a, cudaStream_t s);
 void launch_matfree_mp(const SpmvArgs& a, cudaStream_t s);  // 3D mass, multi-pass (a.mpT1 != null)

@@ -497,6 +497,10 @@ void launch_spmv_fin(const SpmvArgs& a, unsigned int nb, cudaStream_t s) {
 }
 
 void launch_spmv(const SpmvArgs& a, cudaStream_t s) {
+  if (a.sym) {
+    launch_spmv_sym(a, s);
+    return;
+  }
   if (a.mf) {
     launch_matfree(a, s);
     return;
