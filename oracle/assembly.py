@@ -218,6 +218,42 @@ class Discretization:
         return out.reshape(-1)
 
 
+def _element_point_data(ctrl, t, p, n, dim, elem, xg, wg):
+    """Local quadrature data of one element (same definitions as PatchQuad, restricted to the
+    (p+1)^d Gauss points of `elem` and its (p+1)^d non-zero bases, both co-lex, x fastest):
+    weights w|J| (nq,), values B (nq, nloc), physical gradients PD (dim, nq, nloc), and the
+    local basis multi-indices."""
+    h = 1.0 / n
+    V, Dd = [], []
+    for d in range(dim):
+        pts = (elem[d] + 0.5) * h + 0.5 * h * xg
+        sl = slice(elem[d], elem[d] + p + 1)
+        V.append(splines.basis(t, p, pts)[:, sl])
+        Dd.append(splines.basis_deriv(t, p, pts)[:, sl])
+
+    def kron_dirs(mats):  # kron(A_z, kron(A_y, A_x)): x fastest in both points and bases
+        out = mats[0]
+        for A in mats[1:]:
+            out = np.kron(A, out)
+        return out
+
+    B = kron_dirs(V)
+    D = [kron_dirs([Dd[a] if a == c else V[a] for a in range(dim)]) for c in range(dim)]
+    loc = list(itertools.product(*[range(elem[d], elem[d] + p + 1) for d in reversed(range(dim))]))
+    loc = [j[::-1] for j in loc]  # (x, y(, z)), x fastest
+    m = n + p
+    lin = np.array([j[0] + m * (j[1] + (m * j[2] if dim == 3 else 0)) for j in loc])
+    # J[q, a, b] = sum_j C_j[a] dB_j/dxi_b (P:602)
+    J = np.einsum("ja,bqj->qab", ctrl[lin], np.array(D))
+    det = np.linalg.det(J)
+    Ji = np.linalg.inv(J)
+    PD = np.einsum("qca,cqj->aqj", Ji, np.array(D))  # d_a B = sum_c Jinv[c, a] d_xi_c B
+    wq = wg
+    for _ in range(dim - 1):
+        wq = np.kron(wg, wq)
+    return 0.5 ** dim * h ** dim * wq * det, B, PD, loc
+
+
 def operator_rows(ctrl, p, n, dim, rows, omega=1.0):
     """Rows of the unreduced scalar M and K of one patch, computed one by one
     by local quadrature over the support elements of each row (same
@@ -227,8 +263,6 @@ def operator_rows(ctrl, p, n, dim, rows, omega=1.0):
     Used for full-size sampled checks; pinned against patch_operators."""
     t = splines.open_uniform_knots(p, n)
     xg, wg = splines.gauss_legendre(p + 1)
-    m = n + p
-    h = 1.0 / n
     out = {}
     for row in rows:
         row = tuple(int(v) for v in row)
@@ -236,31 +270,44 @@ def operator_rows(ctrl, p, n, dim, rows, omega=1.0):
         ranges = [range(max(0, r - p), min(n, r + 1)) for r in row]
         acc_M, acc_K = {}, {}
         for elem in itertools.product(*ranges):
-            # Gauss points of this element
-            pts1 = [(e + 0.5) * h + 0.5 * h * xg for e in elem]
-            w1 = [0.5 * h * wg for _ in elem]
-            vals = [splines.basis(t, p, pts1[d]) for d in range(dim)]
-            ders = [splines.basis_deriv(t, p, pts1[d]) for d in range(dim)]
-            for qi in itertools.product(range(p + 1), repeat=dim):
-                wq = np.prod([w1[d][qi[d]] for d in range(dim)])
-                # local basis indices of this element: e_d .. e_d + p
-                loc = list(itertools.product(*[range(elem[d], elem[d] + p + 1) for d in range(dim)]))
-                Bv = np.array([np.prod([vals[d][qi[d], j[d]] for d in range(dim)]) for j in loc])
-                Dv = np.array([[np.prod([(ders if d == c else vals)[d][qi[d], j[d]] for d in range(dim)])
-                                for c in range(dim)] for j in loc])
-                lin = [j[0] + m * (j[1] + (m * j[2] if dim == 3 else 0)) for j in loc]
-                J = np.zeros((dim, dim))
-                for jj, L in enumerate(lin):
-                    J += np.outer(ctrl[L], Dv[jj])
-                det = np.linalg.det(J)
-                Ji = np.linalg.inv(J)
-                G = Ji @ Ji.T
-                me = loc.index(row)
-                for jj, j in enumerate(loc):
-                    acc_M[j] = acc_M.get(j, 0.0) + wq * det * Bv[me] * Bv[jj]
-                    acc_K[j] = acc_K.get(j, 0.0) + wq * det * omega ** 2 * (Dv[me] @ G @ Dv[jj])
+            wd, B, PD, loc = _element_point_data(ctrl, t, p, n, dim, elem, xg, wg)
+            me = loc.index(row)
+            mrow = (wd * B[:, me]) @ B
+            krow = omega ** 2 * sum((wd * PD[a][:, me]) @ PD[a] for a in range(dim))
+            for jj, j in enumerate(loc):
+                acc_M[j] = acc_M.get(j, 0.0) + mrow[jj]
+                acc_K[j] = acc_K.get(j, 0.0) + krow[jj]
         cols = sorted(acc_M.keys(), key=lambda j: j[::-1])
         out[row] = (cols, np.array([acc_M[c] for c in cols]), np.array([acc_K[c] for c in cols]))
+    return out
+
+
+def elastic_operator_rows(ctrl, p, n, rows, lam=1.0, mu=1.0):
+    """Rows of the unreduced elastic K of one 3D patch (component-major unknowns), one by one
+    by local quadrature (same definition as patch_operators, ncomp = 3):
+      K_(i,a),(j,b) = sum_q w|J| [lam d_aB_i d_bB_j + mu d_bB_i d_aB_j + mu delta_ab grad B_i . grad B_j].
+    rows: control-point multi-indices (x, y, z).  Returns dict row -> (cols, vals) with
+    vals[c][a][b] = K_(row,a),(cols[c],b).  Used for full-size sampled checks (C4); pinned
+    against patch_operators."""
+    dim = 3
+    t = splines.open_uniform_knots(p, n)
+    xg, wg = splines.gauss_legendre(p + 1)
+    out = {}
+    for row in rows:
+        row = tuple(int(v) for v in row)
+        ranges = [range(max(0, r - p), min(n, r + 1)) for r in row]
+        acc = {}
+        for elem in itertools.product(*ranges):
+            wd, B, PD, loc = _element_point_data(ctrl, t, p, n, dim, elem, xg, wg)
+            me = loc.index(row)
+            gi = wd[None, :] * PD[:, :, me]                 # w|J| d_a B_row at the points (a, q)
+            G = np.einsum("aq,bqj->abj", gi, PD)              # G[a, b, j] = sum_q w|J| d_aB_row d_bB_j
+            lap = np.einsum("aaj->j", G)
+            blk = lam * G + mu * np.transpose(G, (1, 0, 2)) + mu * np.eye(dim)[:, :, None] * lap[None, None, :]
+            for jj, j in enumerate(loc):
+                acc[j] = acc.get(j, 0.0) + blk[:, :, jj]
+        cols = sorted(acc.keys(), key=lambda j: j[::-1])
+        out[row] = (cols, np.array([acc[c] for c in cols]))
     return out
 
 

@@ -296,18 +296,28 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
   return GA_OK;
 }
 
-// op_mode 0: which representation is faster, from the measured operator times
-// (DESIGN.md §6 "Stencil vs matrix-free"); multi-patch grids always use stencils.
-// op_mode 0 (R14, §6 "Stencil vs matrix-free"): measured, the stencil SpMV at
-// 0.8-0.97 of HBM bandwidth beats the fp64-bound sum factorisation at every degree where the
-// stencils fit, so: full stencils if M and K fit in ~150 GB, else half-symmetric stencils
-// (same bytes streamed per apply, half the footprint), else matrix-free.
+// op_mode 0 (R14, §6 "Stencil vs matrix-free", "Symmetric SpMV"): measured per apply.
+// The full stencil SpMV streams its (2p+1)^d coefficients at 0.8-1.0 of HBM bandwidth; the
+// single-read symmetric SpMV (3D scalar, spmv_sym.cu) streams half of them at 0.75-0.88, so it
+// wins wherever its 32-point x-segments are well used (C3 n = 192: p = 2 1.20 -> 0.89 ms,
+// p = 4 6.6 -> 4.2 ms per M apply; n = 96: p = 2, 4, 5 faster) and loses where the last segment
+// is nearly empty at low p (p = 3, n = 96: nx = 97 = 3 x 32 + 1, 0.40 vs 0.44 ms).  So: 3D scalar
+// -> half-symmetric if p >= 4 or the segments are >= 90 % used, else full stencils if they fit
+// in ~150 GB, else half-symmetric, else matrix-free (multi-patch grids: stencils).
 int op_auto(const ga_desc* d) {
   const double W1 = 2.0 * d->p + 1.0, S = d->dim == 3 ? W1 * W1 * W1 : W1 * W1;
   const double npts = std::pow((double)((d->n + d->p - 1) * 2), d->dim);  // generous (multi-patch box)
   const double nsp = d->npatch == 1 ? std::pow((double)(d->n + d->p - 2), d->dim) : npts;
   const double full = 8.0 * S * nsp * (d->ncomp == 3 ? 10.0 : 2.0);
   const double half = 8.0 * nsp * (d->ncomp == 3 ? (S + 1) / 2 + 9 * S : S + 1);
+  if (d->dim == 3 && d->ncomp == 1 && d->npatch == 1) {
+    const int nx = d->n + d->p - 2, nseg = (nx + 31) / 32;
+    const double sym = 2.0 * 8.0 * ((S + 1) / 2) * 32.0 * nseg * (double)nx * nx;  // M + K, segment layout
+    if (sym <= 165e9 && (d->p >= 4 || nx >= 0.9 * 32 * nseg)) return 3;
+    if (full <= 150e9) return 1;
+    if (sym <= 165e9) return 3;
+    return 2;
+  }
   if (full <= 150e9) return 1;
   if (half <= 150e9) return 3;
   return d->npatch == 1 ? 2 : 3;

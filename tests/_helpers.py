@@ -63,6 +63,26 @@ class Case:
         return self.disc.restrict_local(self.prob["u0"])
 
 
+def record_parity(errs, floor=None, bar=None, **extra):
+    """Append one parity result (relative M-norm errors of u, v, a against the oracle, the
+    oracle-vs-oracle floor F, the bar max(1e-10, 10 F)) to the JSON-lines record
+    GA_PARITY_RECORD (default gpurun_out/parity_record.jsonl), committed from the GPU run under
+    profiles/ so the cases that meet 1e-10 outright and those on a widened bar are visible."""
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.environ.get("GA_PARITY_RECORD", os.path.join(root, "gpurun_out", "parity_record.jsonl"))
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    rec = {"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0],
+           "errs_uva": [float(e) for e in errs],
+           "floor_uva": None if floor is None else [float(f) for f in floor],
+           "bar_uva": None if bar is None else [float(b) for b in bar],
+           "meets_1e-10": bool(all(e <= 1e-10 for e in errs))}
+    rec.update(extra)
+    with open(path, "a") as f:
+        f.write(json.dumps(rec) + "\n")
+
+
 def mnorm_rel(M, x, ref):
     e = x - ref
     den = math.sqrt(max(ref @ (M @ ref), 1e-300))

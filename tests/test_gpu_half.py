@@ -10,7 +10,7 @@ import pytest
 import synth
 from oracle import precond
 
-from _helpers import Case, mnorm_rel, oracle_with_floor
+from _helpers import Case, mnorm_rel, oracle_with_floor, record_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -21,11 +21,11 @@ HALF_CASES = {
     "3d_p3_n4_k3": synth.config("c3", p=3, n=4, k=3),
     "3d_p4_n3": synth.config("c3", p=4, n=3),
     "3d_p6_n2": synth.config("c3", p=6, n=2),
-    # the single-read 3D kernel (spmv_sym.cu): several x-segments (nx = 40 -> 2 x 20), y-tiles
-    # and z-chunks; ragged segments (nx = 30 in one 32-wide segment, nx = 18 -> XS = 20)
+    # the single-read 3D kernel (spmv_sym.cu): two x-segments (nx = 40 = 32 + 8), y-tiles and
+    # z-chunks; one ragged segment (nx = 21).  Larger p on multi-segment grids:
+    # test_sym_kernel_equals_full_stencil (the oracle's p = 6 assembly is too slow there)
     "3d_p2_n40": synth.config("c3", p=2, n=40),
-    "3d_p3_n29": synth.config("c3", p=3, n=29),
-    "3d_p6_n14": synth.config("c3", p=6, n=14),
+    "3d_p3_n20": synth.config("c3", p=3, n=20),
     "elastic_p2_n3": synth.config("c4", p=2, n=3),
     "lshape_p2_n4": synth.config("c5", p=2, n=4),
 }
@@ -115,4 +115,7 @@ def test_half_trajectory(cfg, nsteps):
     u, v, a = (c.from_lib(t) for t in c.ctx.get_state())
     ref, floor = oracle_with_floor(d, cfg["k"], cfg["rho"], c.dt, u0, np.zeros_like(u0), nsteps, case=c)
     errs = [mnorm_rel(d.M, x, y) for x, y in zip((u, v, a), ref[:3])]
-    assert all(e < max(1e-10, 10 * f) for e, f in zip(errs, floor)), (errs, floor)
+    bar = [max(1e-10, 10 * f) for f in floor]
+    record_parity(errs, floor, bar, n_free=int(d.nfree * d.ncomp), steps=nsteps, p=cfg["p"], k=cfg["k"],
+                  rho=cfg["rho"], operator_mode=3)
+    assert all(e < b for e, b in zip(errs, bar)), (errs, floor)

@@ -10,7 +10,7 @@ import pytest
 import synth
 from oracle import integrator, precond
 
-from _helpers import Case, mnorm_rel, oracle_with_floor
+from _helpers import Case, mnorm_rel, oracle_with_floor, record_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -22,6 +22,9 @@ OP_CASES = {
     "3d_p3": synth.config("c3", p=3, n=3),
     "3d_p5": synth.config("c3", p=5, n=2),
     "elastic_p2": synth.config("c4", p=2, n=3),
+    # C4's configured degree, and lam != mu (a lam <-> mu swap or a mu-for-2mu slip would show)
+    "elastic_p4": synth.config("c4", p=4, n=2),
+    "elastic_p3_lam2_mu05": synth.config("c4", p=3, n=2, lam=2.0, mu=0.5),
     "lshape_p2": synth.config("c5", p=2, n=4),
     "lshape_p3": synth.config("c5", p=3, n=5),
 }
@@ -102,6 +105,8 @@ def _trajectory(cfg, nsteps, tol=1e-10, v0fac=0.0, **kw):
     ref, floor = oracle_with_floor(d, cfg["k"], cfg["rho"], c.dt, u0, v0, nsteps, ps, case=c)
     errs = [mnorm_rel(d.M, x, y) for x, y in zip((u, v, a), ref[:3])]
     bar = [max(tol, 10 * f) for f in floor]
+    record_parity(errs, floor, bar, n_free=int(d.nfree * d.ncomp), steps=nsteps, p=cfg["p"], k=cfg["k"],
+                  rho=cfg["rho"], operator_mode=c.ctx.operator_mode())
     assert all(e < b for e, b in zip(errs, bar)), (errs, floor)
     return c, errs, st
 
@@ -125,6 +130,19 @@ def test_c3_reduced(p, k, rho):
 
 def test_c4_reduced():
     _trajectory(synth.config("c4", p=2, n=3), 20)
+
+
+@pytest.mark.parametrize("p,n,lam,mu", [(4, 3, 1.0, 1.0), (4, 2, 2.0, 0.5), (3, 4, 0.7, 1.3)],
+                         ids=["p4_n3", "p4_n2_lam2_mu05", "p3_n4_lam07_mu13"])
+def test_c4_configured_degree_and_lame(p, n, lam, mu):
+    # BASELINE configs[3] at its configured p = 4 (reduced n), and with lam != mu
+    _trajectory(synth.config("c4", p=p, n=n, lam=lam, mu=mu), 20)
+
+
+@pytest.mark.parametrize("p,n,k,rho", [(2, 16, 2, 0.0), (3, 12, 2, 0.5), (4, 8, 3, 0.0), (4, 8, 2, 1.0)])
+def test_c3_larger_grids(p, n, k, rho):
+    # C3 trajectories on grids of 1e3-4e3 DoFs per direction product (n = 8-32)
+    _trajectory(synth.config("c3", p=p, n=n, k=k, rho=rho), 40)
 
 
 def test_c5_reduced():
