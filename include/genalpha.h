@@ -69,6 +69,24 @@ typedef struct {
   const double* ctrl;
 } ga_patch;
 
+/* Subdomain of a partitioned multi-patch problem (patch-per-GPU mode): the
+ * context holds ONE patch of a conforming multi-patch domain of any layout (arbitrary patch
+ * orientations, any number of patches at a vertex, e.g. a fan) and its operators are the patch's
+ * LOCAL contributions M^(r), K^(r) (M = sum_r P_r^T M^(r) P_r).  Interface DoFs are
+ * free DoFs of every patch that holds a copy; a ga_group (below) sums the partial values of the
+ * copies after every operator and preconditioner application, so the vectors of all subdomains
+ * stay consistent (equal values on every copy).  Produce the arrays with ga_partition_plan.
+ * All arrays are HOST, (n+p)^dim entries in the patch's co-lexicographic control-point order,
+ * copied by ga_create. */
+typedef struct {
+  const unsigned char* free_mask; /* 1: free DoF of the global problem (not Dirichlet)      */
+  const unsigned char* owned;     /* 1: this subdomain counts the DoF in global norms (one owner   */
+                                  /*    per free DoF across all subdomains)                       */
+  const long long* iface;         /* global interface slot (0..n_iface-1) of a DoF with copies in  */
+                                  /* >= 2 patches, -1 otherwise                                   */
+  long long n_iface;              /* number of interface DoFs of the whole domain (same for all)  */
+} ga_subdomain;
+
 typedef struct {
   int dim;              /* 2 or 3                                                     */
   int ncomp;            /* 1: scalar wave u'' = div(omega^2 grad u);            */
@@ -111,6 +129,10 @@ typedef struct {
   double damp_a0, damp_a1; /* Rayleigh damping C = damp_a0 M + damp_a1 K, >= 0 (SURVEY    */
                         /* NEXT-2; reading R16: block j subtracts C w_j, w_j the Taylor */
                         /* predictor of its velocity-level entry for j < k); 0 0: none  */
+  const ga_subdomain* sub; /* NULL: the context is the whole problem.  Non-NULL: npatch must */
+                        /* be 1 and the context is one subdomain of a partitioned problem */
+                        /* (cell ignored); it is stepped only through a ga_group, op_mode */
+                        /* 2 (matrix-free) and Dirichlet lifting are not available       */
 } ga_desc;
 
 typedef struct {
@@ -262,6 +284,68 @@ int ga_operator_mode(const ga_ctx* ctx);
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream);
 
 void ga_destroy(ga_ctx* ctx);
+
+/* ===========================================================================================
+ * Partitioned multi-patch (patch-per-GPU; additive Schwarz P:763-783)
+ * =========================================================================================== */
+
+/* Partition plan of a conforming multi-patch domain (host only, no GPU).  ctrl[r]: HOST array of
+ * (n+p)^dim control points of patch r (co-lex, dim doubles each).  Gluing: two local
+ * control points are copies of one global function iff their control points are bitwise equal
+ * (conformity); a patch face is an interface iff its control-point set equals a face
+ * of another patch; a global function is Dirichlet iff a copy lies on a face that is not an
+ * interface.  Outputs (caller-allocated, npatch * (n+p)^dim entries, patch-major), the
+ * ga_subdomain arrays of every patch: free_mask, owned (the first copy in (patch, local index)
+ * order owns a free DoF), iface (slots numbered in first-copy order).  *n_iface and
+ * *n_free_global (either may be NULL) receive the interface and free DoF counts.
+ * GA_ERR_ARG: bad sizes / NULL; GA_ERR_CONFORMITY: a face shares some but not all of its points
+ * with another patch's face (non-conforming interface). */
+ga_status ga_partition_plan(int dim, int p, int n, int npatch, const double* const* ctrl,
+                            unsigned char* free_mask, unsigned char* owned, long long* iface,
+                            long long* n_iface, long long* n_free_global);
+
+/* A group steps the subdomain contexts of one partitioned problem together.  The contexts of
+ * this process are passed in ctxs (any number >= 1, all created with a ga_subdomain of the same
+ * plan, the same k, ncomp, dt, rho, PCG settings, all on the current device); the others live in
+ * other processes, one NCCL communicator connecting the processes (nccl_comm from
+ * ga_nccl_comm_init, NULL for a single process).  Per PCG iteration of the lock-stepped solve the
+ * group makes two exchanges (after q = M p and after z = calM^{-1} r): each context writes the
+ * partial values of its interface DoFs and its partial dot products into its exchange buffer,
+ * the buffers of the process are summed in a fixed order, then NCCL all-reduces the sum across
+ * processes (ncclSum, fp64), and every context takes back the sums: q, z stay consistent and all
+ * contexts compute the same alpha, beta and convergence decisions.  p.q and r.z are sums of the
+ * unassembled local products (p^T M p = sum_r p_r^T M^(r) p_r), ||r||^2 and ||b||^2 count every
+ * DoF once (owned mask).  The step is one CUDA graph (PCG loops as conditional WHILE nodes) for
+ * a single process; with NCCL the iteration is a captured graph relaunched by the host, which
+ * polls the convergence flags one iteration behind.
+ * ga_group_create SYNCHRONIZES stream: it sums diag(M) over the copies (D^(r) of P:779 is the
+ * global diagonal, reading R6), sets the preconditioner scalings and builds the graphs. */
+typedef struct ga_group ga_group;
+ga_status ga_group_create(ga_ctx* const* ctxs, int nctx, void* nccl_comm, void* stream, ga_group** out);
+/* ga_set_state of every local context (d_u0[i], d_v0[i] for ctxs[i]; d_v0 or entries may be
+ * NULL): consistent free-DoF vectors of each subdomain (equal values on interface copies). */
+ga_status ga_group_set_state(ga_group* g, const double* const* d_u0, const double* const* d_v0, void* stream);
+ga_status ga_group_advance(ga_group* g, int nsteps, void* stream);
+/* which: 0 = M, 1 = K, 2 = calM_ad^{-1}: y_i = (op x)_i restricted to subdomain i, with
+ * the operators of the whole (glued) problem; x consistent.  For tests / tooling. */
+ga_status ga_group_apply(ga_group* g, int which, const double* const* d_x, double* const* d_y, void* stream);
+/* x = M^{-1} b by the group PCG (zero initial guess); *iters (may be NULL) SYNCHRONIZES. */
+ga_status ga_group_solve_mass(ga_group* g, const double* const* d_b, double* const* d_x, int* iters, void* stream);
+/* Forcing of a subdomain context: as ga_set_forcing, but d_G holds this subdomain's LOCAL load
+ * integrals int_{Omega_r} g B_i (the group sums the copies).  Call before ga_group_set_state. */
+ga_status ga_group_set_forcing(ga_group* g, int i, const double* d_G, int nterms, const double* amp,
+                               const double* omega, const double* phase, double t0, void* stream);
+void ga_group_destroy(ga_group* g);
+/* Last error message of a group call (or of the calling thread's last group call if g is NULL). */
+const char* ga_group_last_error(const ga_group* g);
+
+/* NCCL plumbing for multi-process groups (libnccl.so.2 is loaded at run time: env GA_NCCL_LIB or
+ * the default search path).  ga_nccl_unique_id: rank 0 writes 128 bytes that every rank passes
+ * to ga_nccl_comm_init (the caller moves them, e.g. with torch.distributed.broadcast).
+ * GA_ERR_ARG if NCCL cannot be loaded or fails. */
+ga_status ga_nccl_unique_id(void* id128);
+ga_status ga_nccl_comm_init(int nranks, const void* id128, int rank, void** comm);
+void ga_nccl_comm_destroy(void* comm);
 
 /* Last error message of ctx (or of the calling thread if ctx is NULL). */
 const char* ga_last_error(const ga_ctx* ctx);

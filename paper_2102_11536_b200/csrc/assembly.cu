@@ -199,7 +199,7 @@ __global__ void k_contract_final(const double* __restrict__ in, const double* __
   long long grow = 0, gcol_ok = 1, rmul = 1;
   int gr[3], gc[3];
   for (int d = 0; d < DIM; ++d) {
-    gr[d] = f.cell[d] * (m - 1) + ii[d] - 1;
+    gr[d] = f.cell[d] * (m - 1) + ii[d] - f.org[d];
     gc[d] = gr[d] + oo[d];
     if (gr[d] < 0 || gr[d] >= f.G[d]) return;
     if (gc[d] < 0 || gc[d] >= f.G[d]) gcol_ok = 0;

@@ -29,6 +29,7 @@ struct ContractDesc {
 struct FinalDesc {
   int W1, m, p, n, qoff, r0, r1;
   int cell[3];
+  int org[3];                  // grid coordinate = cell (m - 1) + local index - org (1: Dirichlet ring)
   int G[3];
   long long npts;
   long long S;                 // offsets per coefficient array

@@ -8,6 +8,7 @@ namespace ga {
 constexpr int KMAX = 4;           // max blocks k (right-hand sides per lock-stepped solve)
 constexpr int NTHREADS = 256;     // default block size for grid kernels
 constexpr int MAXPATCH = 16;
+constexpr int XSCAL = 4 * KMAX;  // scalars of a subdomain exchange (dist.cu): up to 2 KMAX sums + spare
 
 // Device-resident PCG scalars of one lock-stepped solve set.
 struct PcgState {

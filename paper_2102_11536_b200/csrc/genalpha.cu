@@ -21,80 +21,13 @@
 
 using namespace ga;
 
+#include "ctx.cuh"
+
 namespace {
-
 thread_local std::string g_thread_err;
-
-struct PatchHost {
-  int cell[3];
-  std::vector<double> ctrl;
-};
-
-struct PrecPatch {
-  int lo[3], bd[3];     // box in grid coordinates
-  int llo[3];           // first local basis index per direction
-  double* s = nullptr;  // device, box points
-  double* t = nullptr;  // device, nvec*box*k (multi-patch only)
-  double* L[3] = {nullptr, nullptr, nullptr};
-  double* Ff[3] = {nullptr, nullptr, nullptr};
-  double* Fb[3] = {nullptr, nullptr, nullptr};
-  int clen[3] = {0, 0, 0}, nchunk[3] = {0, 0, 0}, nlev[3] = {0, 0, 0};
-  std::vector<double> hL[3], hdiag[3];
-  SweepFactor sf[3], sb[3];
-};
-
 }  // namespace
 
-struct ga_ctx {
-  ga_desc d{};
-  std::vector<PatchHost> patches;
-  int dim = 2, nvec = 1, p = 1, n = 1, m = 2, k = 1, W1 = 3;
-  long long S = 0;
-  GridDesc g{};
-  long long nfree = 0;  // scalar free DoFs
-  std::vector<long long> hmap;           // api -> grid (multi-patch)
-  std::vector<unsigned char> hmask;      // grid mask (multi-patch)
-  std::vector<long long> hlocal;         // api -> patch*m^dim + local
-  double alpha[KMAX], beta[KMAX], gamma[KMAX], alpha_f[KMAX], theta_max = 0;
-  // device views into the workspace
-  char* ws = nullptr;
-  size_t ws_bytes = 0;
-  double *coefM = nullptr, *coefK = nullptr, *chain = nullptr;
-  double *pred = nullptr, *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr, *pv1 = nullptr;
-  unsigned char* mask = nullptr;
-  long long* map = nullptr;
-  PcgState* pcg = nullptr;
-  DevStatus* st = nullptr;
-  double* partial = nullptr;
-  unsigned int* counter = nullptr;
-  double* dscal = nullptr;  // small device scalars
-  std::vector<PrecPatch> prec;
-  // graphs
-  cudaStream_t aux = nullptr, cap = nullptr;  // private capture streams
-  cudaGraphExec_t g_step = nullptr, g_solveK = nullptr, g_solveB = nullptr;
-  cudaGraph_t gr_step = nullptr, gr_solveK = nullptr, gr_solveB = nullptr;
-  std::string err;
-  bool nograph = false;  // GA_NO_GRAPH=1: direct launches, host-driven PCG loop (profiling/debug)
-  bool persist = false;  // small single-patch scalar problems: one cooperative kernel per solve
-  bool mf = false;       // matrix-free M (and scalar K): sum factorisation from Gauss-point data
-  bool half = false;     // half-symmetric stencils (offsets o >= 0, zero guard of g.guard rows)
-  bool sym = false;      // 3D scalar half stencils in the segment-blocked layout (spmv_sym.cu)
-  double* symzero = nullptr;  // zero block read by the single-read SpMV for unstored rows
-  SymLayout sl = {0, 0};
-  double *mfWM = nullptr, *mfWK = nullptr, *mftv = nullptr, *mftd = nullptr, *diagM = nullptr;
-  double *mpT1 = nullptr, *mpT2 = nullptr, *mpT3 = nullptr;  // 3D multi-pass mass intermediates
-  // forcing F = G h(t) (ga_set_forcing): grid vector, device slot table, host parameters
-  double* forceG = nullptr;
-  ForceSlots* fslots = nullptr;
-  bool forcing = false;       // any pair active (pair 0 ga_set_forcing, 1-2 ga_set_dirichlet)
-  double *lzv = nullptr, *lzab = nullptr;  // Lanczos vectors and alpha/beta (ga_lambda_max)
-  int fnterms[FMAXPAIRS] = {0, 0, 0};
-  double famp[FMAXPAIRS][FMAXTERMS], fomega[FMAXPAIRS][FMAXTERMS], fphase[FMAXPAIRS][FMAXTERMS], ft0 = 0.0;
-  long long mfws = 0;    // Gauss points (n(p+1))^dim
-  long long* trace = nullptr;  // GA_TRACE=1: persistent-solver phase timestamps (debug)
-};
-
-namespace {
+namespace gaint {
 
 #define CK(call)                                                                    \
   do {                                                                              \
@@ -115,7 +48,7 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
   size_t off_coefM, off_coefK, off_symzero, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
       off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots,
-      off_lz, off_lzab;
+      off_lz, off_lzab, off_xgi, off_xslot, off_xinv, off_xbuf, off_xrecv;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
   size_t total;
 };
@@ -135,6 +68,10 @@ struct Shape {
   bool half = false;   // half-symmetric stencils (op_mode 3, or auto)
   bool sym = false;    // ... in the segment-blocked layout of the single-read 3D SpMV (scalar, 3D)
   SymLayout sl = {0, 0};
+  int org[3] = {1, 1, 1};  // local control-point index of grid coordinate 0
+  bool sub = false;        // subdomain of a partitioned problem (make_shape_sub)
+  long long n_iface = 0;
+  std::vector<int> xgi, xslot;  // held interface DoFs: grid index, global slot
 };
 
 int op_auto(const ga_desc* d);
@@ -158,6 +95,13 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
     return GA_ERR_ARG;
   }
   if (d->op_mode == 2 && d->npatch != 1) { seterr(ctx, "op_mode 2 (matrix-free) supports a single patch"); return GA_ERR_ARG; }
+  if (d->sub) {
+    if (d->npatch != 1 || !d->sub->free_mask || !d->sub->owned || !d->sub->iface || d->sub->n_iface < 0) {
+      seterr(ctx, "subdomain: npatch 1 and free_mask, owned, iface arrays required");
+      return GA_ERR_ARG;
+    }
+    if (d->op_mode == 2) { seterr(ctx, "subdomain: op_mode 2 (matrix-free) is not available"); return GA_ERR_ARG; }
+  }
   double a[KMAX], b[KMAX], g[KMAX], f[KMAX], th;
   int rc = scheme_params(d->k, d->rho_b, d->rho_s, d->param_set, a, b, g, f, &th);
   if (rc != 0) { seterr(ctx, "invalid rho_b/rho_s (need 0 <= rho_s <= rho_b <= 1; param_set 1 needs rho < 1)"); return GA_ERR_PARAM; }
@@ -174,6 +118,65 @@ ga_status validate(const ga_desc* d, ga_ctx* ctx) {
   return GA_OK;
 }
 
+// Subdomain grid (ga_desc.sub): the bounding box [lo, hi] of the patch's free control points;
+// grid coordinate = local index - lo (org = lo); mask 1 = free and owned, 2 = free copy owned by
+// another subdomain, 0 = Dirichlet point inside the box (e.g. the re-entrant corner of an
+// L-shape patch); one preconditioner box = the grid, local basis range [lo, hi] (reading R6:
+// zero extension of the non-tensor free set to its bounding box).
+ga_status make_shape_sub(const ga_desc* d, Shape& sh, ga_ctx* ctx) {
+  const int m = sh.m, dim = sh.dim;
+  const long long mpow = dim == 3 ? (long long)m * m * m : (long long)m * m;
+  const ga_subdomain* sd = d->sub;
+  sh.sym = false;  // the single-read 3D SpMV assumes a full box; masked grids use the two-pass half kernel
+  int lo[3] = {m, m, m}, hi[3] = {-1, -1, -1};
+  for (long long i = 0; i < mpow; ++i) {
+    if (!sd->free_mask[i]) continue;
+    const int li[3] = {(int)(i % m), (int)((i / m) % m), dim == 3 ? (int)(i / ((long long)m * m)) : 0};
+    for (int c = 0; c < dim; ++c) { lo[c] = std::min(lo[c], li[c]); hi[c] = std::max(hi[c], li[c]); }
+  }
+  if (hi[0] < 0) { seterr(ctx, "subdomain has no free DoF"); return GA_ERR_ARG; }
+  int G[3] = {1, 1, 1};
+  for (int c = 0; c < dim; ++c) { G[c] = hi[c] - lo[c] + 1; sh.org[c] = lo[c]; }
+  sh.g.dim = dim; sh.g.nx = G[0]; sh.g.ny = G[1]; sh.g.nz = dim == 3 ? G[2] : 1;
+  sh.g.npts = (long long)sh.g.nx * sh.g.ny * sh.g.nz;
+  long long guard = (long long)sh.p * (1 + sh.g.nx + (dim == 3 ? (long long)sh.g.nx * sh.g.ny : 0));
+  guard = (guard + 32 + 31) / 32 * 32;
+  sh.g.guard = guard;
+  sh.g.padded = sh.g.npts + 2 * guard;
+  sh.g.cs = (sh.g.npts + 31) / 32 * 32;
+  sh.sl = sym_layout(sh.g.nx);
+  sh.mask.assign(sh.g.npts, 0);
+  sh.map.clear();
+  sh.local.clear();
+  sh.xgi.clear();
+  sh.xslot.clear();
+  for (long long gi = 0; gi < sh.g.npts; ++gi) {
+    const int gc[3] = {(int)(gi % sh.g.nx), (int)((gi / sh.g.nx) % sh.g.ny), (int)(gi / ((long long)sh.g.nx * sh.g.ny))};
+    long long loc = 0, mul = 1;
+    for (int c = 0; c < dim; ++c) { loc += (long long)(gc[c] + lo[c]) * mul; mul *= m; }
+    if (!sd->free_mask[loc]) continue;
+    sh.mask[gi] = sd->owned[loc] ? 1 : 2;
+    sh.map.push_back(gi);
+    sh.local.push_back(loc);
+    if (sd->iface[loc] >= 0) {
+      if (sd->iface[loc] >= sd->n_iface) { seterr(ctx, "subdomain: interface slot out of range"); return GA_ERR_ARG; }
+      sh.xgi.push_back((int)gi);
+      sh.xslot.push_back((int)sd->iface[loc]);
+    }
+  }
+  sh.nfree = (long long)sh.map.size();
+  sh.prec.clear();
+  PrecPatch pp;
+  for (int c = 0; c < 3; ++c) {
+    if (c >= dim) { pp.lo[c] = 0; pp.bd[c] = 1; pp.llo[c] = 0; continue; }
+    pp.lo[c] = 0; pp.bd[c] = G[c]; pp.llo[c] = lo[c];
+  }
+  sh.prec.push_back(pp);
+  sh.sub = true;
+  sh.n_iface = sd->n_iface;
+  return GA_OK;
+}
+
 // Global masked grid, boxes, maps.
 ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_conformity) {
   sh.dim = d->dim; sh.nvec = d->ncomp; sh.p = d->p; sh.n = d->n; sh.m = d->n + d->p; sh.k = d->k; sh.W1 = 2 * d->p + 1;
@@ -185,6 +188,8 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
   sh.sym = sh.half && d->dim == 3 && d->ncomp == 1;
   sh.S = (long long)sh.W1 * sh.W1 * (sh.dim == 3 ? sh.W1 : 1);
   const int m = sh.m, dim = sh.dim;
+  for (int c = 0; c < 3; ++c) sh.org[c] = 1;
+  if (d->sub) return make_shape_sub(d, sh, ctx);
   int cmax[3] = {0, 0, 0};
   for (int i = 0; i < d->npatch; ++i)
     for (int c = 0; c < dim; ++c) cmax[c] = std::max(cmax[c], d->patches[i].cell[c]);
@@ -306,6 +311,10 @@ ga_status make_shape(const ga_desc* d, Shape& sh, ga_ctx* ctx, bool check_confor
 // in ~150 GB, else half-symmetric, else matrix-free (multi-patch grids: stencils).
 int op_auto(const ga_desc* d) {
   const double W1 = 2.0 * d->p + 1.0, S = d->dim == 3 ? W1 * W1 * W1 : W1 * W1;
+  if (d->sub) {  // subdomain: full stencils unless they do not fit (the masked-grid rule below)
+    const double nsub = std::pow((double)(d->n + d->p), d->dim);
+    return 8.0 * S * nsub * (d->ncomp == 3 ? 10.0 : 2.0) <= 150e9 ? 1 : 3;
+  }
   const double npts = std::pow((double)((d->n + d->p - 1) * 2), d->dim);  // generous (multi-patch box)
   const double nsp = d->npatch == 1 ? std::pow((double)(d->n + d->p - 2), d->dim) : npts;
   const double full = 8.0 * S * nsp * (d->ncomp == 3 ? 10.0 : 2.0);
@@ -355,7 +364,7 @@ Layout make_layout(const Shape& sh) {
     L.off_mfWM = take(sh.mf ? sizeof(double) * nqd : 0);
     L.off_mfWK = take(mfK ? sizeof(double) * nqd * (sh.dim == 3 ? 6 : 3) : 0);
     L.off_mftab = take(sh.mf ? sizeof(double) * 2 * nq * (sh.p + 1) : 0);
-    L.off_diag = take(sh.mf ? sizeof(double) * npts : 0);
+    L.off_diag = take((sh.mf || sh.sub) ? sizeof(double) * npts : 0);
     // multi-pass 3D mass intermediates (matfree_mp.cu)
     const bool mp = sh.mf && sh.dim == 3;
     const long long nfd = sh.g.nx;
@@ -365,7 +374,7 @@ Layout make_layout(const Shape& sh) {
   }
   L.off_chain = take(sizeof(double) * 3 * sh.k * sh.nvec * sh.g.padded);
   for (int i = 0; i < 8; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
-  const bool multi = sh.prec.size() > 1;
+  const bool multi = sh.prec.size() > 1 || sh.sub;
   L.off_mask = take(multi ? npts : 0);
   L.off_map = take(multi ? sizeof(long long) * sh.nfree : 0);
   L.off_pcg = take(sizeof(PcgState));
@@ -388,6 +397,13 @@ Layout make_layout(const Shape& sh) {
   L.off_fslots = take(sizeof(ForceSlots));
   L.off_lz = take(sizeof(double) * 2 * sh.nvec * sh.g.padded * sh.k);  // Lanczos v_{j-1}, v_j (MV layout)
   L.off_lzab = take(sizeof(double) * 2 * (LZMAX + 2));
+  // subdomain exchange: held interface lists, slot -> grid index, send and receive buffers
+  const long long xcount = sh.sub ? (long long)sh.nvec * sh.n_iface * sh.k + XSCAL : 0;
+  L.off_xgi = take(sizeof(int) * sh.xgi.size());
+  L.off_xslot = take(sizeof(int) * sh.xslot.size());
+  L.off_xinv = take(sh.sub ? sizeof(int) * sh.n_iface : 0);
+  L.off_xbuf = take(sizeof(double) * xcount);
+  L.off_xrecv = take(sizeof(double) * xcount);
   for (size_t r = 0; r < sh.prec.size(); ++r) {
     const PrecPatch& pp = sh.prec[r];
     long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
@@ -509,6 +525,7 @@ VecArgs vec_args(ga_ctx* c) {
   a.tol2 = c->d.pcg_rtol * c->d.pcg_rtol;
   a.x = c->x; a.r = c->r; a.z = c->z; a.p = c->pv; a.b = c->b;
   a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
+  a.own = nullptr; a.xsum = nullptr;
   return a;
 }
 
@@ -776,7 +793,7 @@ ga_status assemble(ga_ctx* ctx, const Shape& sh, char* scratch, size_t scratch_b
         FinalDesc f;
         memset(&f, 0, sizeof(f));
         f.W1 = W1; f.m = m; f.p = p; f.n = n; f.qoff = qa; f.r0 = r0; f.r1 = r1;
-        for (int d = 0; d < 3; ++d) f.cell[d] = ctx->patches[r].cell[d];
+        for (int d = 0; d < 3; ++d) { f.cell[d] = ctx->sub ? 0 : ctx->patches[r].cell[d]; f.org[d] = ctx->org[d]; }
         f.G[0] = sh.g.nx; f.G[1] = sh.g.ny; f.G[2] = sh.g.nz;
         f.npts = sh.g.cs;
         f.S = sh.S;
@@ -888,7 +905,9 @@ ga_status run_kind(ga_ctx* ctx, GraphKind kind, cudaStream_t s) {
   return GA_OK;
 }
 
-}  // namespace
+}  // namespace gaint
+
+using namespace gaint;
 
 // ===========================================================================
 // C ABI
@@ -922,6 +941,46 @@ ga_status ga_query(const ga_desc* desc, size_t* n_free, size_t* workspace_bytes,
   if (scratch_bytes) *scratch_bytes = std::max(smin, std::min(sall, cap));
   return GA_OK;
 }
+
+}  // extern "C"
+
+// diag(M) of the local operator from the stencil centre (subdomain contexts)
+__global__ void k_centre(double* diag, long long npts, const double* coefM, long long S, long long hguard) {
+  const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= npts) return;
+  const long long hr = gi + hguard;
+  diag[gi] = hguard >= 0 ? coefM[((hr >> 5) * ((S + 1) / 2)) * 32 + (hr & 31)]
+                         : coefM[((gi >> 5) * S + S / 2) * 32 + (gi & 31)];
+}
+
+namespace gaint {
+ga_status compute_scaling(ga_ctx* ctx, cudaStream_t s) {
+  for (size_t r = 0; r < ctx->prec.size(); ++r) {
+    PrecPatch& pp = ctx->prec[r];
+    const long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
+    // 1D diagonals of the parametric mass go to the q vector temporarily
+    double* tmp = ctx->q;
+    const double* dd[3] = {nullptr, nullptr, nullptr};
+    size_t o = 0;
+    for (int d = 0; d < ctx->dim; ++d) {
+      CK(cudaMemcpyAsync(tmp + o, pp.hdiag[d].data(), sizeof(double) * pp.bd[d], cudaMemcpyHostToDevice, s));
+      dd[d] = tmp + o;
+      o += pp.bd[d];
+    }
+    k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
+                                                                 pp.lo[2], dd[0], dd[1], ctx->dim == 3 ? dd[2] : nullptr,
+                                                                 ctx->coefM, ctx->diagM, ctx->S, ctx->g.nx, ctx->g.ny,
+                                                                 ctx->mask, ctx->half ? ctx->g.guard : -1,
+                                                                 ctx->sym ? ctx->sl : SymLayout{0, 0});
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));  // tmp reused by the next patch
+  }
+  CK(cudaMemsetAsync(ctx->q, 0, sizeof(double) * ctx->nvec * ctx->g.padded * ctx->k, s));
+  return GA_OK;
+}
+}  // namespace gaint
+
+extern "C" {
 
 ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_bytes, void* d_scratch,
                     size_t scratch_bytes, void* stream, ga_ctx** out) {
@@ -983,7 +1042,20 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->chain = (double*)(ws + L.off_chain);
   double** mv[8] = {&ctx->pred, &ctx->b, &ctx->x, &ctx->r, &ctx->z, &ctx->pv, &ctx->q, &ctx->pv1};
   for (int i = 0; i < 8; ++i) *mv[i] = (double*)(ws + L.off_mv[i]);
-  const bool multi = desc->npatch > 1;
+  const bool multi = desc->npatch > 1 || sh.sub;
+  ctx->sub = sh.sub;
+  for (int c = 0; c < 3; ++c) ctx->org[c] = sh.org[c];
+  if (sh.sub) {
+    ctx->n_iface = sh.n_iface;
+    ctx->nxl = (long long)sh.xgi.size();
+    ctx->xgi = (int*)(ws + L.off_xgi);
+    ctx->xslot = (int*)(ws + L.off_xslot);
+    ctx->xinv = (int*)(ws + L.off_xinv);
+    ctx->xcount = (long long)sh.nvec * sh.n_iface * sh.k + XSCAL;
+    ctx->xbuf = (double*)(ws + L.off_xbuf);
+    ctx->xrecv = (double*)(ws + L.off_xrecv);
+    ctx->diagM = (double*)(ws + L.off_diag);
+  }
   ctx->mask = multi ? (unsigned char*)(ws + L.off_mask) : nullptr;
   ctx->map = multi ? (long long*)(ws + L.off_map) : nullptr;
   ctx->pcg = (PcgState*)(ws + L.off_pcg);
@@ -1014,6 +1086,18 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     CKD(cudaMemcpyAsync(ctx->mask, sh.mask.data(), sh.g.npts, cudaMemcpyHostToDevice, s));
     CKD(cudaMemcpyAsync(ctx->map, sh.map.data(), sizeof(long long) * sh.nfree, cudaMemcpyHostToDevice, s));
   }
+  std::vector<int> hxinv;
+  if (sh.sub) {
+    hxinv.assign((size_t)sh.n_iface, -1);
+    for (size_t i = 0; i < sh.xgi.size(); ++i) hxinv[(size_t)sh.xslot[i]] = sh.xgi[i];
+    if (!sh.xgi.empty()) {
+      CKD(cudaMemcpyAsync(ctx->xgi, sh.xgi.data(), sizeof(int) * sh.xgi.size(), cudaMemcpyHostToDevice, s));
+      CKD(cudaMemcpyAsync(ctx->xslot, sh.xslot.data(), sizeof(int) * sh.xslot.size(), cudaMemcpyHostToDevice, s));
+    }
+    if (!hxinv.empty()) CKD(cudaMemcpyAsync(ctx->xinv, hxinv.data(), sizeof(int) * hxinv.size(), cudaMemcpyHostToDevice, s));
+    CKD(cudaMemsetAsync(ctx->xbuf, 0, sizeof(double) * 2 * ctx->xcount, s));
+    CKD(cudaStreamSynchronize(s));  // hxinv is a stack vector
+  }
   if (sh.mf) {  // 1D basis tables of the matrix-free apply (host_math.cpp)
     Tables1D T0 = make_tables(sh.p, sh.n);
     CKD(cudaMemcpyAsync(ctx->mftv, T0.val.data(), sizeof(double) * T0.val.size(), cudaMemcpyHostToDevice, s));
@@ -1032,10 +1116,8 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   ctx->prec = sh.prec;
   for (size_t r = 0; r < ctx->prec.size(); ++r) {
     PrecPatch& pp = ctx->prec[r];
-    long long nbox = (long long)pp.bd[0] * pp.bd[1] * pp.bd[2];
     pp.s = (double*)(ws + L.off_s[r]);
     pp.t = multi ? (double*)(ws + L.off_t[r]) : nullptr;
-    double* dd[3] = {nullptr, nullptr, nullptr};
     for (int d = 0; d < 3; ++d) {
       pp.L[d] = (double*)(ws + L.off_L[d][r]);
       if (d >= sh.dim) continue;
@@ -1072,25 +1154,15 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       CKD(cudaMemcpyAsync(pp.Ff[d], pp.sf[d].buf.data(), sizeof(double) * pp.sf[d].buf.size(), cudaMemcpyHostToDevice, s));
       CKD(cudaMemcpyAsync(pp.Fb[d], pp.sb[d].buf.data(), sizeof(double) * pp.sb[d].buf.size(), cudaMemcpyHostToDevice, s));
       CKD(cudaMemcpyAsync(pp.L[d], pp.hL[d].data(), sizeof(double) * Lf.size(), cudaMemcpyHostToDevice, s));
-      dd[d] = ctx->dscal;  // placeholder, replaced below
     }
-    // 1D diagonals go to the t area temporarily (single patch: x MV is free now)
-    double* tmp = ctx->q;
-    size_t o = 0;
-    for (int d = 0; d < sh.dim; ++d) {
-      CKD(cudaMemcpyAsync(tmp + o, pp.hdiag[d].data(), sizeof(double) * pp.bd[d], cudaMemcpyHostToDevice, s));
-      dd[d] = tmp + o;
-      o += pp.bd[d];
-    }
-    const double* center = ctx->coefM;  // blocked layout: k_scaling indexes offset S/2
-    k_scaling<<<(unsigned int)((nbox + 255) / 256), 256, 0, s>>>(pp.s, pp.bd[0], pp.bd[1], pp.bd[2], pp.lo[0], pp.lo[1],
-                                                                 pp.lo[2], dd[0], dd[1], sh.dim == 3 ? dd[2] : nullptr,
-                                                                 center, ctx->diagM, ctx->S, sh.g.nx, sh.g.ny, ctx->mask,
-                                                                 sh.half ? sh.g.guard : -1,
-                                                                 sh.sym ? sh.sl : SymLayout{0, 0});
-    CKD(cudaGetLastError());
-    CKD(cudaStreamSynchronize(s));  // tmp reused by the next patch
   }
+  if (sh.sub) {  // local diag(M) (the group sums the interface copies and recomputes the scalings)
+    k_centre<<<(unsigned int)((sh.g.npts + 255) / 256), 256, 0, s>>>(ctx->diagM, sh.g.npts, ctx->coefM, ctx->S,
+                                                                    sh.half ? sh.g.guard : -1);
+    CKD(cudaGetLastError());
+  }
+  rc = compute_scaling(ctx, s);
+  if (rc != GA_OK) { ga_destroy(ctx); return rc; }
   CKD(cudaMemsetAsync(ctx->q, 0, sizeof(double) * sh.nvec * sh.g.padded * sh.k, s));
   // graphs
   // graphs are captured on a private stream (the caller's may be the legacy stream)
@@ -1101,14 +1173,15 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     // latency-bound regime: little data per PCG phase (C2-like); bandwidth-bound grids keep the graph path
     const bool small = (long long)sh.g.npts * sh.k <= 600000 && (double)sh.S * sh.g.npts * 8.0 <= 64e6;
     const bool want = pe ? (*pe != '0') : small;
-    ctx->persist = want && !ctx->mf && !ctx->half && persist_supported(persist_args(ctx));
+    ctx->persist = want && !ctx->mf && !ctx->half && !ctx->sub && persist_supported(persist_args(ctx));
+    if (ctx->sub) ctx->nograph = true;  // subdomains are stepped by their ga_group (dist.cu)
     const char* te = getenv("GA_TRACE");
     if (te && *te && *te != '0') {
       cudaMalloc(&ctx->trace, 8192 * sizeof(long long));  // debug only
       cudaMemset(ctx->trace, 0, 8192 * sizeof(long long));
     }
   }
-  if (!ctx->nograph) {
+  if (!ctx->nograph && !ctx->sub) {
     rc = build_graph(ctx, ctx->cap, GK_STEP, &ctx->gr_step, &ctx->g_step);
     if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEK, &ctx->gr_solveK, &ctx->g_solveK);
     if (rc == GA_OK) rc = build_graph(ctx, ctx->cap, GK_SOLVEB, &ctx->gr_solveB, &ctx->g_solveB);
@@ -1155,18 +1228,35 @@ __global__ void k_reset_status(DevStatus* st, PcgState* pc, int keep_time) {
   memset(pc, 0, sizeof(PcgState));
 }
 
+}  // extern "C"
+
+namespace gaint {
 // keep_time: the simulation step index (forcing clock) survives, e.g. ga_set_chain on a resume
-static void reset_status(ga_ctx* ctx, cudaStream_t s, int keep_time = 0) {
+void reset_status(ga_ctx* ctx, cudaStream_t s, int keep_time) {
   k_reset_status<<<1, 1, 0, s>>>(ctx->st, ctx->pcg, keep_time);
 }
+
+}  // namespace gaint
+
+extern "C" {
 
 static ga_status check_ctx(ga_ctx* ctx) {
   if (!ctx) { seterr(nullptr, "ctx is NULL"); return GA_ERR_ARG; }
   return GA_OK;
 }
 
+// entry points that step or solve need the whole problem: a subdomain goes through its ga_group
+static ga_status check_whole(ga_ctx* ctx) {
+  if (!ctx) { seterr(nullptr, "ctx is NULL"); return GA_ERR_ARG; }
+  if (ctx->sub) { seterr(ctx, "subdomain context: step and solve through its ga_group"); return GA_ERR_ARG; }
+  return GA_OK;
+}
+
+}  // extern "C"
+
+namespace gaint {
 // step slot table: block j (slot j-1) takes F^{(3j-3)} at t_n + alpha_fj dt (eq:ho1)
-static ga_status set_step_slots(ga_ctx* ctx, cudaStream_t s) {
+ga_status set_step_slots(ga_ctx* ctx, cudaStream_t s) {
   if (!ctx->forcing) return GA_OK;
   ForceSlots fs;
   memset(&fs, 0, sizeof(fs));
@@ -1175,7 +1265,7 @@ static ga_status set_step_slots(ga_ctx* ctx, cudaStream_t s) {
   return GA_OK;
 }
 
-static ga_status set_predictors_and_norm(ga_ctx* ctx, cudaStream_t s) {
+ga_status set_predictors_and_norm(ga_ctx* ctx, cudaStream_t s) {
   {
     ga_status rc = set_step_slots(ctx, s);
     if (rc != GA_OK) return rc;
@@ -1190,8 +1280,12 @@ static ga_status set_predictors_and_norm(ga_ctx* ctx, cudaStream_t s) {
   return GA_OK;
 }
 
+}  // namespace gaint
+
+extern "C" {
+
 ga_status ga_set_state(ga_ctx* ctx, const double* d_u0, const double* d_v0, void* stream) {
-  ga_status rc = check_ctx(ctx);
+  ga_status rc = check_whole(ctx);
   if (rc != GA_OK) return rc;
   if (!d_u0) { seterr(ctx, "u0 is NULL"); return GA_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
@@ -1281,7 +1375,7 @@ ga_status ga_set_dirichlet(ga_ctx* ctx, const double* h_g, int nterms, const dou
   if (rc != GA_OK) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const bool on = h_g != nullptr && nterms > 0;
-  if (on && (ctx->patches.size() != 1 || ctx->nvec != 1)) {
+  if (on && (ctx->patches.size() != 1 || ctx->nvec != 1 || ctx->sub)) {
     seterr(ctx, "Dirichlet lifting: single patch, scalar wave only");
     return GA_ERR_ARG;
   }
@@ -1329,7 +1423,7 @@ ga_status ga_set_dirichlet(ga_ctx* ctx, const double* h_g, int nterms, const dou
 }
 
 ga_status ga_advance(ga_ctx* ctx, int nsteps, void* stream) {
-  ga_status rc = check_ctx(ctx);
+  ga_status rc = check_whole(ctx);
   if (rc != GA_OK) return rc;
   if (nsteps < 0) { seterr(ctx, "nsteps < 0"); return GA_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
@@ -1411,7 +1505,7 @@ ga_status ga_get_stats(ga_ctx* ctx, ga_stats* out, void* stream) {
 }
 
 ga_status ga_profile_op(ga_ctx* ctx, int op, int reps, void* stream) {
-  ga_status rc = check_ctx(ctx);
+  ga_status rc = check_whole(ctx);
   if (rc != GA_OK) return rc;
   if (op < 0 || op > 6 || reps < 0) { seterr(ctx, "bad op"); return GA_ERR_ARG; }
   if (op == 6) {
@@ -1482,7 +1576,7 @@ ga_status ga_apply(ga_ctx* ctx, int which, const double* d_x, double* d_y, void*
 }
 
 ga_status ga_solve_mass(ga_ctx* ctx, const double* d_b, double* d_x, int* iters, void* stream) {
-  ga_status rc = check_ctx(ctx);
+  ga_status rc = check_whole(ctx);
   if (rc != GA_OK) return rc;
   if (!d_b || !d_x) { seterr(ctx, "NULL vector"); return GA_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
@@ -1509,7 +1603,7 @@ ga_status ga_lambda_max(ga_ctx* ctx, int iters, double* lam, void* stream) {
   // lambda_max(M^{-1} K) by Lanczos in the M inner product: each step
   // one K apply + one PCG mass solve (the K-solve graph) + one M apply; the alpha/beta stay on
   // the device, the largest eigenvalue of the tridiagonal matrix is found on the host
-  ga_status rc = check_ctx(ctx);
+  ga_status rc = check_whole(ctx);
   if (rc != GA_OK) return rc;
   if (iters < 1 || !lam) { seterr(ctx, "iters >= 1 and lam required"); return GA_ERR_ARG; }
   iters = std::min(iters, LZMAX);

@@ -634,17 +634,24 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
         }
       }
     }
+    // subdomain (a.xsum): r.z over every local DoF (z_r unassembled: r.z = sum_r r_r . z_r),
+    // r.r over the owned DoFs only (each global DoF once)
+    const double wr = (a.xsum && a.mask && a.mask[i] != 1) ? 0.0 : 1.0;
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
       a.z[base + j] = z[j];
       const double r = a.r[base + j];
       v[j] = fma(r, z[j], v[j]);
-      v[KK + j] = fma(r, r, v[KK + j]);
+      v[KK + j] = fma(wr * r, r, v[KK + j]);
     }
   }
   if (dead) return;
   double out[2 * KK];
   if (reduce_last_block<2 * KK>(v, a.partial, a.counter, out)) {
+    if (a.xsum) {
+      for (int j = 0; j < 2 * KK; ++j) a.xsum[j] = out[j];
+      return;
+    }
     double rz[KMAX], rr[KMAX];
     for (int j = 0; j < KK; ++j) { rz[j] = out[j]; rr[j] = out[KK + j]; }
     pcg_finalize(a.pcg, a.st, KK, a.maxit, a.cond, rz, rr);
@@ -887,17 +894,22 @@ __global__ void __launch_bounds__(NTHREADS) k_init_from_b(VecArgs a) {
     const int c = (int)(e / npts);
     const int i = (int)e - c * npts;
     const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+    const double wb = (a.own && a.own[i] != 1) ? 0.0 : 1.0;  // subdomain: owned DoFs only
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
       const double b = a.b[base + j];
       a.r[base + j] = b;
       a.x[base + j] = 0.0;
-      v[j] = fma(b, b, v[j]);
+      v[j] = fma(wb * b, b, v[j]);
     }
   }
   if (dead) return;
   double out[KK];
   if (reduce_last_block<KK>(v, a.partial, a.counter, out)) {
+    if (a.xsum) {
+      for (int j = 0; j < KK; ++j) a.xsum[j] = out[j];
+      return;
+    }
     PcgState* pc = a.pcg;
     pc->iter = 0; pc->first = 1; pc->pfirst = 1; pc->nrhs = KK; pc->phase = 0; pc->guard = 0;
     for (int j = 0; j < KK; ++j) {

@@ -53,6 +53,9 @@ struct SpmvArgs {
   // 3D matrix-free mass by the multi-pass non-redundant sum factorisation (matfree_mp.cu):
   // intermediates T1 [c][n_q][nf][nf][k], T2 / T3 [c][n_q][n_q][nf][k]
   double *mpT1, *mpT2, *mpT3;
+  // subdomain group (dist.cu): SPMV_PQ writes its local p.q sums here (k_spmv_fin) instead of
+  // taking the PCG scalar step, which runs after the exchange (null: ordinary context)
+  double* xsum;
 };
 void launch_spmv(const SpmvArgs& a, cudaStream_t s);
 void launch_spmv_sym(const SpmvArgs& a, cudaStream_t s);  // a.sym = 1 (spmv_sym.cu)
@@ -90,6 +93,9 @@ struct PrecArgs {
   int maxit;
   unsigned long long cond;        // graph conditional handle (0: none)
   int update;                     // apply x += alpha p, r -= alpha q first (if !pcg->first)
+  // subdomain group (dist.cu): k_prec_out writes its local sums [r.z (kk) | owned r.r (kk)] here
+  // and skips the scalar step (run after the exchange); null: ordinary context
+  double* xsum;
 };
 void launch_precond(const PrecArgs& a, cudaStream_t s);
 // 3D single patch: the three direction sweeps as shared-memory slabs (slab.cu); false if a
@@ -105,6 +111,10 @@ struct VecArgs {
   DevStatus* st;
   double* partial;
   unsigned int* counter;
+  // subdomain group (dist.cu): k_init_from_b writes the owned ||b||^2 (mask value 1) here and
+  // leaves the PcgState set-up to the step after the exchange; null: ordinary context
+  const unsigned char* own;
+  double* xsum;
 };
 void launch_init_from_b(const VecArgs& a, cudaStream_t s);
 void launch_p_update(const VecArgs& a, cudaStream_t s);

@@ -339,6 +339,11 @@ __global__ void __launch_bounds__(1024) k_spmv_fin(SpmvArgs a, unsigned int nblo
     for (int j = 0; j < KK; ++j) acc[j] += a.partial[(size_t)b * KK + j];
   block_sum<KK>(acc);
   if (threadIdx.x != 0) return;
+  if (a.xsum && a.mode == SPMV_PQ) {  // subdomain: local p.q to the exchange (dist.cu)
+#pragma unroll
+    for (int j = 0; j < KK; ++j) a.xsum[j] = acc[j];
+    return;
+  }
   PcgState* pc = a.pcg;
   if (a.mode == SPMV_PQ) {
     pc->iter += 1;

@@ -25,11 +25,18 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_ARG", -2: "GA_ERR_PARAM", -3: "GA_ERR_GE
 EXPORTED = ["ga_params", "ga_spectral_scan", "ga_query", "ga_create", "ga_set_state", "ga_set_forcing", "ga_set_time", "ga_set_dirichlet", "ga_advance", "ga_get_state",
             "ga_get_chain", "ga_set_chain", "ga_get_stats", "ga_apply", "ga_solve_mass",
             "ga_lambda_max", "ga_free_dof_map", "ga_profile_op", "ga_uses_persistent_solver", "ga_uses_matrix_free", "ga_operator_mode", "ga_destroy",
-            "ga_last_error"]
+            "ga_last_error", "ga_partition_plan", "ga_group_create", "ga_group_set_state", "ga_group_advance",
+            "ga_group_apply", "ga_group_solve_mass", "ga_group_set_forcing", "ga_group_destroy", "ga_group_last_error",
+            "ga_nccl_unique_id", "ga_nccl_comm_init", "ga_nccl_comm_destroy"]
 
 
 class ga_patch(ctypes.Structure):
     _fields_ = [("cell", c_int * 3), ("ctrl", POINTER(c_double))]
+
+
+class ga_subdomain(ctypes.Structure):
+    _fields_ = [("free_mask", POINTER(ctypes.c_ubyte)), ("owned", POINTER(ctypes.c_ubyte)),
+                ("iface", POINTER(c_longlong)), ("n_iface", c_longlong)]
 
 
 class ga_desc(ctypes.Structure):
@@ -39,7 +46,7 @@ class ga_desc(ctypes.Structure):
                 ("rho_s", c_double), ("param_set", c_int), ("dt", c_double), ("pcg_rtol", c_double),
                 ("pcg_maxit", c_int), ("pcg_refine", c_int), ("pcg_refine_rtol", c_double),
                 ("unstable_factor", c_double), ("op_mode", c_int), ("damp_a0", c_double),
-                ("damp_a1", c_double)]
+                ("damp_a1", c_double), ("sub", POINTER(ga_subdomain))]
 
 
 class ga_stats(ctypes.Structure):
@@ -85,6 +92,19 @@ def _load():
         "ga_operator_mode": (c_int, [c_void_p]),
         "ga_destroy": (None, [c_void_p]),
         "ga_last_error": (ctypes.c_char_p, [c_void_p]),
+        "ga_partition_plan": (c_int, [c_int, c_int, c_int, c_int, POINTER(P), c_void_p, c_void_p, c_void_p,
+                                      POINTER(c_longlong), POINTER(c_longlong)]),
+        "ga_group_create": (c_int, [POINTER(c_void_p), c_int, c_void_p, c_void_p, POINTER(c_void_p)]),
+        "ga_group_set_state": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), c_void_p]),
+        "ga_group_advance": (c_int, [c_void_p, c_int, c_void_p]),
+        "ga_group_apply": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_void_p), c_void_p]),
+        "ga_group_solve_mass": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_int), c_void_p]),
+        "ga_group_set_forcing": (c_int, [c_void_p, c_int, c_void_p, c_int, P, P, P, c_double, c_void_p]),
+        "ga_group_destroy": (None, [c_void_p]),
+        "ga_group_last_error": (ctypes.c_char_p, [c_void_p]),
+        "ga_nccl_unique_id": (c_int, [c_void_p]),
+        "ga_nccl_comm_init": (c_int, [c_int, c_void_p, c_int, POINTER(c_void_p)]),
+        "ga_nccl_comm_destroy": (None, [c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -127,9 +147,11 @@ def spectral_scan(theta, k, rho_b, rho_s=None, param_set=0):
 
 def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3, param_set=0,
               omega=1.0, lam=1.0, mu=1.0, density=1.0, pcg_rtol=1e-13, pcg_maxit=500,
-              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6, op_mode=0, damp_a0=0.0, damp_a1=0.0):
+              pcg_refine=None, pcg_refine_rtol=None, unstable_factor=1e6, op_mode=0, damp_a0=0.0, damp_a1=0.0,
+              sub=None):
     """ga_desc from [(cell, ctrl ndarray (m^dim, dim))].  Keeps the ctrl arrays
-    alive on the returned object (`_keep`)."""
+    alive on the returned object (`_keep`).  sub: a Subdomain of a PartitionPlan (one patch)
+    for the partitioned (patch-per-GPU) mode, stepped through a Group."""
     arr = (ga_patch * len(patches))()
     keep = []
     for i, (cell, ctrl) in enumerate(patches):
@@ -146,7 +168,13 @@ def make_desc(patches, p, n, dim, *, ncomp=1, k=2, rho=0.5, rho_s=None, dt=1e-3,
                 pcg_refine=(1 if p >= 5 else 0) if pcg_refine is None else pcg_refine,
                 pcg_refine_rtol=(1e-3 if p >= 5 else 0.0) if pcg_refine_rtol is None else pcg_refine_rtol,
                 unstable_factor=unstable_factor, op_mode=op_mode, damp_a0=damp_a0, damp_a1=damp_a1)
-    d._keep = (arr, keep)
+    sd = None
+    if sub is not None:
+        sd = ga_subdomain(free_mask=sub.free_mask.ctypes.data_as(POINTER(ctypes.c_ubyte)),
+                          owned=sub.owned.ctypes.data_as(POINTER(ctypes.c_ubyte)),
+                          iface=sub.iface.ctypes.data_as(POINTER(c_longlong)), n_iface=int(sub.n_iface))
+        d.sub = ctypes.pointer(sd)
+    d._keep = (arr, keep, sd, sub)
     return d
 
 
@@ -287,6 +315,127 @@ class Context:
         out = (c_longlong * (self.n_free // ncomp))()
         _check(lib.ga_free_dof_map(self.ctx, out))
         return np.frombuffer(out, dtype=np.int64).copy()
+
+
+# --------------------------------------------------------------------------- partitioned multi-patch
+class Subdomain:
+    """ga_subdomain arrays of one patch (host numpy, (n+p)^dim entries, co-lex)."""
+
+    def __init__(self, free_mask, owned, iface, n_iface):
+        self.free_mask = np.ascontiguousarray(free_mask, dtype=np.uint8)
+        self.owned = np.ascontiguousarray(owned, dtype=np.uint8)
+        self.iface = np.ascontiguousarray(iface, dtype=np.int64)
+        self.n_iface = int(n_iface)
+
+
+class PartitionPlan:
+    """ga_partition_plan of a conforming multi-patch domain: .sub[r] (Subdomain of patch r),
+    .n_iface, .n_free (global free DoFs)."""
+
+    def __init__(self, ctrls, p, n, dim):
+        m = n + p
+        mp = m ** dim
+        cs = [np.ascontiguousarray(c, dtype=np.float64).reshape(-1) for c in ctrls]
+        for c in cs:
+            assert c.size == mp * dim
+        arr = (POINTER(c_double) * len(cs))(*[c.ctypes.data_as(POINTER(c_double)) for c in cs])
+        fm = np.zeros(len(cs) * mp, dtype=np.uint8)
+        ow = np.zeros(len(cs) * mp, dtype=np.uint8)
+        it = np.zeros(len(cs) * mp, dtype=np.int64)
+        ni, nf = c_longlong(), c_longlong()
+        _check(lib.ga_partition_plan(int(dim), int(p), int(n), len(cs), arr, c_void_p(fm.ctypes.data),
+                                     c_void_p(ow.ctypes.data), c_void_p(it.ctypes.data), byref(ni), byref(nf)))
+        self.n_iface, self.n_free = ni.value, nf.value
+        self.sub = [Subdomain(fm[r * mp:(r + 1) * mp], ow[r * mp:(r + 1) * mp], it[r * mp:(r + 1) * mp], ni.value)
+                    for r in range(len(cs))]
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.ga_nccl_unique_id(ctypes.cast(buf, c_void_p)))
+    return buf.raw
+
+
+def nccl_comm_init(nranks, uid: bytes, rank):
+    buf = ctypes.create_string_buffer(uid, 128)
+    comm = c_void_p()
+    _check(lib.ga_nccl_comm_init(int(nranks), ctypes.cast(buf, c_void_p), int(rank), byref(comm)))
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    lib.ga_nccl_comm_destroy(comm)
+
+
+def _gerr(g):
+    return lib.ga_group_last_error(g).decode(errors="replace")
+
+
+def _gcheck(code, g=None):
+    if code != GA_OK:
+        raise GAError(code, _gerr(g))
+
+
+class Group:
+    """ga_group over subdomain Contexts of this process (one NCCL communicator for the other
+    processes of a multi-GPU run, None on one process).  Vectors are lists (one torch tensor
+    per context, its free-DoF order)."""
+
+    def __init__(self, contexts, nccl_comm=None, stream=None):
+        import torch
+        self.torch = torch
+        self.ctxs = list(contexts)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        arr = (c_void_p * len(self.ctxs))(*[c.ctx for c in self.ctxs])
+        g = c_void_p()
+        _gcheck(lib.ga_group_create(arr, len(self.ctxs), nccl_comm, c_void_p(self.stream.cuda_stream), byref(g)))
+        self.g = g
+
+    def _s(self):
+        return c_void_p(self.stream.cuda_stream)
+
+    @staticmethod
+    def _arr(ts):
+        return (c_void_p * len(ts))(*[None if t is None else _ptr(t) for t in ts])
+
+    def close(self):
+        if getattr(self, "g", None):
+            lib.ga_group_destroy(self.g)
+            self.g = None
+
+    __del__ = close
+
+    def set_state(self, u0s, v0s=None):
+        _gcheck(lib.ga_group_set_state(self.g, self._arr(u0s), self._arr(v0s) if v0s is not None else None,
+                                       self._s()), self.g)
+
+    def set_forcing(self, i, G=None, terms=(), t0=0.0):
+        """Forcing of context i: G its LOCAL load integrals (free-DoF tensor), terms (a, w, phi)."""
+        n = len(terms) if G is not None else 0
+        arr = [(c_double * max(1, n))(*[t[q] for t in terms]) for q in range(3)]
+        _gcheck(lib.ga_group_set_forcing(self.g, int(i), _ptr(G) if G is not None else None, n, arr[0], arr[1],
+                                         arr[2], float(t0), self._s()), self.g)
+
+    def advance(self, nsteps):
+        _gcheck(lib.ga_group_advance(self.g, int(nsteps), self._s()), self.g)
+
+    def apply(self, which, xs):
+        ys = [c.vec() for c in self.ctxs]
+        _gcheck(lib.ga_group_apply(self.g, {"M": 0, "K": 1, "Pinv": 2}.get(which, which), self._arr(xs),
+                                   self._arr(ys), self._s()), self.g)
+        return ys
+
+    def solve_mass(self, bs):
+        xs = [c.vec() for c in self.ctxs]
+        it = c_int(-1)
+        _gcheck(lib.ga_group_solve_mass(self.g, self._arr(bs), self._arr(xs), byref(it), self._s()), self.g)
+        return xs, it.value
+
+    def get_state(self):
+        return [c.get_state() for c in self.ctxs]
+
+    def stats(self):
+        return [c.stats() for c in self.ctxs]
 
 
 def _aligned(t):

@@ -23,7 +23,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "greville_1d", "control_net", "lshape_patches", "sine_modes", "eval_modes",
+    "greville_1d", "control_net", "lshape_patches", "fan_patches", "sine_modes", "eval_modes",
     "sinpi_product", "e1_exact", "CONFIGS", "config", "make_problem",
 ]
 
@@ -81,6 +81,52 @@ def lshape_patches(p: int, n: int, noise: float, seed: int):
     return out
 
 
+def fan_patches(dim: int, p: int, n: int, npatch: int = 7, noise: float = 0.0, seed: int = 0,
+                radius: float = 1.0, height: float = 1.0):
+    """A fan of npatch (>= 3) kite-shaped patches around the origin (a
+    generator standing in for the paper's seven-blade fan, whose CAD is not available).
+
+    Patch r has the corners O = 0 (xi = eta = 0), A = R e(theta_r) (xi = 1), B = R e(theta_r +
+    pi / npatch) (xi = eta = 1) and C = R e(theta_{r+1}) (eta = 1), theta_j = 2 pi j / npatch: its
+    control points are the bilinear map of the Greville grid.  Neighbours share a ray edge with
+    rotated parameter directions (patch r's eta axis = patch r+1's xi axis), all npatch patches
+    share the centre vertex.  dim 3: the fan extruded over z in [0, height] (Greville in z), all
+    patches share the centre axis.  Ray edges / faces are evaluated by one expression in both
+    patches (bitwise-equal control points, conformity P:645-652); interior points get U(-a h, a h)
+    noise per coordinate (h = radius / n), one PCG64 stream in patch order.  Returns
+    [((r, 0, 0)[:dim], ctrl)]."""
+    assert npatch >= 3
+    m = n + p
+    g = greville_1d(p, n)
+    ray = [radius * np.array([np.cos(2 * np.pi * j / npatch), np.sin(2 * np.pi * j / npatch)])
+           for j in range(npatch)]
+    rng = np.random.default_rng(seed)
+    h = radius / n
+    out = []
+    for r in range(npatch):
+        A, C = ray[r], ray[(r + 1) % npatch]
+        tb = 2 * np.pi * (r + 0.5) / npatch
+        B = radius * np.array([np.cos(tb), np.sin(tb)])
+        xi, eta = np.meshgrid(g, g, indexing="xy")  # [eta][xi], xi fastest
+        xy = (xi * (1 - eta))[..., None] * A + (xi * eta)[..., None] * B + ((1 - xi) * eta)[..., None] * C
+        xy[0, :, :] = g[:, None] * A[None, :]      # eta = 0 edge: shared with patch r-1
+        xy[:, 0, :] = g[:, None] * C[None, :]      # xi = 0 edge: shared with patch r+1
+        xy[0, 0, :] = 0.0
+        pts2 = xy.reshape(-1, 2)
+        if dim == 2:
+            pts = pts2.copy()
+            idx = np.indices((m, m)).reshape(2, -1)[::-1]
+        else:
+            gz = g * height
+            pts = np.concatenate([np.tile(pts2, (m, 1)), np.repeat(gz, m * m)[:, None]], axis=1)
+            idx = np.indices((m, m, m)).reshape(3, -1)[::-1]
+        interior = np.all((idx > 0) & (idx < m - 1), axis=0)
+        delta = rng.uniform(-noise * h, noise * h, size=pts.shape)
+        pts[interior] += delta[interior]
+        out.append(((r, 0, 0)[:dim], np.ascontiguousarray(pts)))
+    return out
+
+
 def sine_modes(seed: int, nmodes: int = 8) -> np.ndarray:
     """Amplitudes a_m ~ N(0,1)/m^2, m = 1..nmodes."""
     rng = np.random.default_rng(seed)
@@ -121,6 +167,12 @@ CONFIGS = {
     # (P:831 read as sin(10 pi y)); u0 = sin sin, v0 = 10 sqrt2 pi sin sin
     "e1": dict(name="e1", dim=2, ncomp=1, p=7, n=100, noise=0.0, seed=1, init="e1",
                init_seed=0, k=2, rho=0.0, steps=100, cfl_frac=0.5, lshape=False, T=0.1),
+    # SURVEY §8f NEXT-4 (patch-per-GPU multi-patch): seven-patch fans, rotated interfaces, seven
+    # patches at the centre vertex (2D) / axis (3D); stand-ins for the paper's fan
+    "fan2d": dict(name="fan2d", dim=2, ncomp=1, p=3, n=256, noise=0.1, seed=6, init="modes",
+                  init_seed=106, k=2, rho=0.3, steps=100, cfl_frac=0.5, lshape=False, fan=7),
+    "fan3d": dict(name="fan3d", dim=3, ncomp=1, p=2, n=48, noise=0.1, seed=7, init="modes",
+                  init_seed=107, k=2, rho=0.3, steps=50, cfl_frac=0.5, lshape=False, fan=7),
 }
 
 
@@ -145,6 +197,8 @@ def make_problem(cfg: dict):
     dim, p, n = cfg["dim"], cfg["p"], cfg["n"]
     if cfg.get("lshape"):
         patches = lshape_patches(p, n, cfg["noise"], cfg["seed"])
+    elif cfg.get("fan"):
+        patches = fan_patches(dim, p, n, cfg["fan"], cfg["noise"], cfg["seed"])
     else:
         patches = [((0,) * dim, control_net(dim, p, n, cfg["noise"], cfg["seed"]))]
     ncomp = cfg.get("ncomp", 1)
