@@ -28,8 +28,9 @@ struct PrecPatch {
   double* L[3] = {nullptr, nullptr, nullptr};
   double* Ff[3] = {nullptr, nullptr, nullptr};
   double* Fb[3] = {nullptr, nullptr, nullptr};
+  double* E[3] = {nullptr, nullptr, nullptr};   // make_seq rows (device)
   int clen[3] = {0, 0, 0}, nchunk[3] = {0, 0, 0}, nlev[3] = {0, 0, 0};
-  std::vector<double> hL[3], hdiag[3];
+  std::vector<double> hL[3], hdiag[3], hE[3];
   SweepFactor sf[3], sb[3];
 };
 

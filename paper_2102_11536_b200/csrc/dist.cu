@@ -237,6 +237,12 @@ struct ga_group {
   cudaStream_t cap = nullptr, aux = nullptr;
   cudaEvent_t ev_fork = nullptr;
   std::vector<cudaEvent_t> ev_join;
+  // a second fork/join set for the capture of the WHILE body (stream aux): the streams of the
+  // first set are still part of the outer capture (stream cap) while the body is captured, and a
+  // stream cannot join two captures
+  std::vector<cudaStream_t> st2;
+  cudaEvent_t ev_fork2 = nullptr;
+  std::vector<cudaEvent_t> ev_join2;
   cudaGraphExec_t g_step = nullptr, g_solveK = nullptr, g_solveB = nullptr;
   cudaGraph_t gr_step = nullptr, gr_solveK = nullptr, gr_solveB = nullptr;
   bool host_loop = false;  // NCCL: the PCG loop is driven by the host (flags polled)
@@ -266,13 +272,17 @@ template <class F>
 ga_status par(ga_group* G, cudaStream_t s, F f) {
   const int R = (int)G->c.size();
   if (R == 1) { f(G->c[0], s); return GA_OK; }
-  GCK(cudaEventRecord(G->ev_fork, s));
+  const bool body = (s == G->aux);
+  const std::vector<cudaStream_t>& st = body ? G->st2 : G->st;
+  const std::vector<cudaEvent_t>& ej = body ? G->ev_join2 : G->ev_join;
+  cudaEvent_t ef = body ? G->ev_fork2 : G->ev_fork;
+  GCK(cudaEventRecord(ef, s));
   for (int r = 0; r < R; ++r) {
-    GCK(cudaStreamWaitEvent(G->st[r], G->ev_fork, 0));
-    f(G->c[r], G->st[r]);
-    GCK(cudaEventRecord(G->ev_join[r], G->st[r]));
+    GCK(cudaStreamWaitEvent(st[r], ef, 0));
+    f(G->c[r], st[r]);
+    GCK(cudaEventRecord(ej[r], st[r]));
   }
-  for (int r = 0; r < R; ++r) GCK(cudaStreamWaitEvent(s, G->ev_join[r], 0));
+  for (int r = 0; r < R; ++r) GCK(cudaStreamWaitEvent(s, ej[r], 0));
   return GA_OK;
 }
 
@@ -580,11 +590,16 @@ ga_status ga_group_create(ga_ctx* const* ctxs, int nctx, void* nccl_comm_p, void
   } while (0)
   G->st.resize(nctx, nullptr);
   G->ev_join.resize(nctx, nullptr);
+  G->st2.resize(nctx, nullptr);
+  G->ev_join2.resize(nctx, nullptr);
   for (int r = 0; r < nctx; ++r) {
     GCKF(cudaStreamCreateWithFlags(&G->st[r], cudaStreamNonBlocking));
     GCKF(cudaEventCreateWithFlags(&G->ev_join[r], cudaEventDisableTiming));
+    GCKF(cudaStreamCreateWithFlags(&G->st2[r], cudaStreamNonBlocking));
+    GCKF(cudaEventCreateWithFlags(&G->ev_join2[r], cudaEventDisableTiming));
   }
   GCKF(cudaEventCreateWithFlags(&G->ev_fork, cudaEventDisableTiming));
+  GCKF(cudaEventCreateWithFlags(&G->ev_fork2, cudaEventDisableTiming));
   GCKF(cudaStreamCreateWithFlags(&G->cap, cudaStreamNonBlocking));
   GCKF(cudaStreamCreateWithFlags(&G->aux, cudaStreamNonBlocking));
   for (ga_ctx* c : G->c) c->grp = G;
@@ -761,6 +776,11 @@ void ga_group_destroy(ga_group* G) {
   for (cudaEvent_t e : G->ev_join)
     if (e) cudaEventDestroy(e);
   if (G->ev_fork) cudaEventDestroy(G->ev_fork);
+  for (cudaStream_t t : G->st2)
+    if (t) cudaStreamDestroy(t);
+  for (cudaEvent_t e : G->ev_join2)
+    if (e) cudaEventDestroy(e);
+  if (G->ev_fork2) cudaEventDestroy(G->ev_fork2);
   if (G->cap) cudaStreamDestroy(G->cap);
   if (G->aux) cudaStreamDestroy(G->aux);
   delete G;

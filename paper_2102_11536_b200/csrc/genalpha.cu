@@ -23,6 +23,37 @@ using namespace ga;
 
 #include "ctx.cuh"
 
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
+namespace {
+// GA_BACKTRACE=1: print the native stack on SIGSEGV (debug aid; offsets resolve with addr2line)
+void ga_segv_handler(int sig) {
+  void* fr[64];
+  const int n = backtrace(fr, 64);
+  backtrace_symbols_fd(fr, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct GaSegvInit {
+  GaSegvInit() {
+    const char* e = getenv("GA_BACKTRACE");
+    if (e && *e == '1') {
+      static char alt[1 << 16];
+      stack_t ss;
+      ss.ss_sp = alt; ss.ss_size = sizeof(alt); ss.ss_flags = 0;
+      sigaltstack(&ss, nullptr);
+      struct sigaction sa;
+      memset(&sa, 0, sizeof(sa));
+      sa.sa_handler = ga_segv_handler;
+      sa.sa_flags = SA_ONSTACK;
+      sigaction(SIGSEGV, &sa, nullptr);
+    }
+  }
+} ga_segv_init;
+}  // namespace
+
 namespace {
 thread_local std::string g_thread_err;
 }  // namespace
@@ -49,7 +80,7 @@ struct Layout {
   size_t off_coefM, off_coefK, off_symzero, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
       off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots,
       off_lz, off_lzab, off_xgi, off_xslot, off_xinv, off_xbuf, off_xrecv;
-  std::vector<size_t> off_s, off_t, off_L[3], off_F[3];
+  std::vector<size_t> off_s, off_t, off_L[3], off_F[3], off_E[3];
   size_t total;
 };
 
@@ -383,13 +414,18 @@ Layout make_layout(const Shape& sh) {
   // tile kernels can launch more blocks than the grid kernels on small grids
   // grid kernels, SpMV (32 rows/block), persistent solver (2 x 1184 blocks, double-buffered)
   long long maxblocks = std::max(std::max((sh.nvec * npts + NTHREADS - 1) / NTHREADS, (npts + 31) / 32), 2LL * 1184) + 1;
+  long long sumt[3] = {0, 0, 0};
   for (const PrecPatch& pp : sh.prec) {
     const long long nb0 = pp.bd[0], nb1 = pp.bd[1], nb2 = pp.bd[2];
-    const long long xt = (sh.nvec * nb1 * nb2 * sh.k + 7) / 8;            // x lines, 8 slots per tile
-    const long long yt = sh.nvec * nb2 * ((nb0 * sh.k + 7) / 8);           // y lines
-    const long long zt = sh.nvec * nb1 * ((nb0 * sh.k + 7) / 8);           // z lines
+    // >= 4 slots per tile (line_seq.cu; the chunked tiles use >= 8)
+    const long long xt = (sh.nvec * nb1 * nb2 * sh.k + 3) / 4;            // x lines
+    const long long yt = sh.nvec * nb2 * ((nb0 * sh.k + 3) / 4);           // y lines
+    const long long zt = sh.nvec * nb1 * ((nb0 * sh.k + 3) / 4);           // z lines
     maxblocks = std::max(maxblocks, std::max(xt, std::max(yt, zt)) + 1);
+    sumt[0] += xt; sumt[1] += yt; sumt[2] += zt;
   }
+  // the tiles of all patches in one launch (additive Schwarz, fused epilogue of line_seq.cu)
+  maxblocks = std::max(maxblocks, std::max(sumt[0], std::max(sumt[1], sumt[2])) + 1);
   L.off_partial = take(sizeof(double) * 2 * KMAX * maxblocks);
   L.off_counter = take(sizeof(unsigned int) * 16);
   L.off_dscal = take(sizeof(double) * 16);
@@ -411,6 +447,7 @@ Layout make_layout(const Shape& sh) {
     L.off_t.push_back(take(multi ? sizeof(double) * sh.nvec * nbox * sh.k : 0));
     for (int c = 0; c < 3; ++c) L.off_L[c].push_back(take(sizeof(double) * (pp.bd[c] + sh.p + 1) * (sh.p + 1)));
     for (int c = 0; c < 3; ++c) L.off_F[c].push_back(take(2 * sweep_bytes(pp.bd[c], sh.p)));
+    for (int c = 0; c < 3; ++c) L.off_E[c].push_back(take(sizeof(double) * 2 * pp.bd[c] * seq_row(sh.p)));
   }
   L.total = o;
   return L;
@@ -476,6 +513,7 @@ PrecArgs prec_args(ga_ctx* c, unsigned long long cond, int update) {
       a.lo[r][d] = c->prec[r].lo[d]; a.bd[r][d] = c->prec[r].bd[d]; a.L[r][d] = c->prec[r].L[d];
       a.Ff[r][d] = (d < c->dim) ? c->prec[r].Ff[d] : nullptr;
       a.Fb[r][d] = (d < c->dim) ? c->prec[r].Fb[d] : nullptr;
+      a.E[r][d] = (d < c->dim) ? c->prec[r].E[d] : nullptr;
       a.clen[r][d] = c->prec[r].clen[d]; a.nchunk[r][d] = c->prec[r].nchunk[d]; a.nlev[r][d] = c->prec[r].nlev[d];
       a.flen[r][d] = (int)c->prec[r].sf[d].buf.size();
     }
@@ -1154,6 +1192,9 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
       CKD(cudaMemcpyAsync(pp.Ff[d], pp.sf[d].buf.data(), sizeof(double) * pp.sf[d].buf.size(), cudaMemcpyHostToDevice, s));
       CKD(cudaMemcpyAsync(pp.Fb[d], pp.sb[d].buf.data(), sizeof(double) * pp.sb[d].buf.size(), cudaMemcpyHostToDevice, s));
       CKD(cudaMemcpyAsync(pp.L[d], pp.hL[d].data(), sizeof(double) * Lf.size(), cudaMemcpyHostToDevice, s));
+      pp.hE[d] = make_seq(Lf, pp.bd[d], sh.p);
+      pp.E[d] = (double*)(ws + L.off_E[d][r]);
+      CKD(cudaMemcpyAsync(pp.E[d], pp.hE[d].data(), sizeof(double) * pp.hE[d].size(), cudaMemcpyHostToDevice, s));
     }
   }
   if (sh.sub) {  // local diag(M) (the group sums the interface copies and recomputes the scalings)
@@ -1163,6 +1204,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   }
   rc = compute_scaling(ctx, s);
   if (rc != GA_OK) { ga_destroy(ctx); return rc; }
+  line_seq_prepare(sh.p);
   CKD(cudaMemsetAsync(ctx->q, 0, sizeof(double) * sh.nvec * sh.g.padded * sh.k, s));
   // graphs
   // graphs are captured on a private stream (the caller's may be the legacy stream)

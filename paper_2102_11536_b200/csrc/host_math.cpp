@@ -222,6 +222,24 @@ int scheme_params(int k, double rb, double rs, int param_set,
 
 namespace ga {
 
+std::vector<double> make_seq(const std::vector<double>& Lr, int n, int p) {
+  const int PP = seq_row(p);
+  std::vector<double> E((size_t)2 * n * PP, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double* f = &E[(size_t)i * PP];
+    const double d = Lr[(size_t)i * (p + 1)];
+    f[0] = d;
+    for (int u = 1; u <= p; ++u) f[u] = (i - u >= 0) ? Lr[(size_t)i * (p + 1) + u] * d : 0.0;
+    // reversed index i: original row io = n-1-i, z_io = (y_io - sum_u L_{io+u,io} z_{io+u}) / L_{io,io}
+    double* b = &E[((size_t)n + i) * PP];
+    const int io = n - 1 - i;
+    const double db = Lr[(size_t)io * (p + 1)];
+    b[0] = db;
+    for (int u = 1; u <= p; ++u) b[u] = (io + u < n) ? Lr[(size_t)(io + u) * (p + 1) + u] * db : 0.0;
+  }
+  return E;
+}
+
 SweepFactor make_sweep(const std::vector<double>& Lr, int n, int p, bool backward, int chunks_target) {
   SweepFactor F;
   F.n = n; F.p = p;

@@ -60,4 +60,12 @@ struct SweepFactor {
 // written as a forward sweep on the reversed line.
 SweepFactor make_sweep(const std::vector<double>& Lrows, int n, int p, bool backward, int chunks_target = 32);
 
+// Sequential form of both sweeps for the whole-line shared-memory solver (line_seq.cu): the
+// divisions are folded into the band, y_i = t_i d_i - sum_{u=1..p} e_{i,u} y_{i-u} with
+// e_{i,u} = c_{i,u} d_i, so one FMA per element is on the recurrence's critical path.
+// Layout (doubles): forward rows [n][PP] = {d_i, e_{i,1..p}, 0 pad}, then the backward rows of the
+// reversed line [n][PP]; PP = seq_row(p) (p + 1 rounded up to even: 16-byte rows).
+inline int seq_row(int p) { return (p + 2) & ~1; }
+std::vector<double> make_seq(const std::vector<double>& Lrows, int n, int p);
+
 }  // namespace ga

@@ -808,6 +808,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
           tl.nrows = a.nvec * nother; tl.nr2 = nother; tl.sA = sc; tl.sB = (g.dim == 3) ? str[other] : 0;
         }
       }
+      if (ok && launch_line_seq_multi(a, d, s)) continue;
       if (ok) ok = tile_multi_dispatch(a.p, m, s);
     }
     if (ok) {

@@ -81,6 +81,7 @@ struct PrecArgs {
   const double* Ff[MAXPATCH][3];  // chunked sweep factors (host_math.h SweepFactor), forward
   const double* Fb[MAXPATCH][3];  // and backward (reversed line)
   int clen[MAXPATCH][3], nchunk[MAXPATCH][3], nlev[MAXPATCH][3], flen[MAXPATCH][3];
+  const double* E[MAXPATCH][3];   // sequential sweep rows (host_math.h make_seq), whole-line solver
   const unsigned char* mask;      // grid mask (nullptr: all free)
   // PCG vectors (MV)
   double *x, *r, *z;
@@ -101,6 +102,11 @@ void launch_precond(const PrecArgs& a, cudaStream_t s);
 // 3D single patch: the three direction sweeps as shared-memory slabs (slab.cu); false if a
 // line set does not fit in shared memory (caller falls back to the streamed sweeps)
 bool launch_precond_slab(const PrecArgs& a, cudaStream_t s);
+// direction d of every patch box by the whole-line shared-memory solver (line_seq.cu); false if
+// not applicable (caller uses the chunked tiles)
+bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s);
+int line_seq_mode();  // GA_LINE_SEQ=0: off (the chunked tiles instead)
+bool line_seq_prepare(int p);  // function attributes of degree p's kernel, outside stream capture
 
 struct VecArgs {
   GridDesc g;
