@@ -369,7 +369,7 @@ bool line_seq_prepare(int p) {
 }
 
 template <int P>
-static bool seq_launch(SeqMulti m, cudaStream_t s) {
+static bool seq_launch(SeqMulti m, cudaStream_t s, bool dry) {
   constexpr int PP = (P + 2) & ~1;
   static int nsm = 0;
   if (!nsm) {
@@ -420,6 +420,7 @@ static bool seq_launch(SeqMulti m, cudaStream_t s) {
   }
   m.tstart[m.np] = t0;
   const size_t sm = smem_for(TS);
+  if (dry) return true;
   k_line_seq<P><<<(unsigned int)t0, 128, sm, s>>>(m);
   return true;
 }
@@ -437,21 +438,29 @@ int line_seq_mode() {
   return mode;
 }
 
-bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s) {
+// Single patch (a.t[0] == nullptr): the lines of the z vector itself (the box is the whole grid).
+// dry: only report whether the launch is possible.
+bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s, bool dry) {
   if (!line_seq_mode()) return false;
   const GridDesc& g = a.g;
+  const bool single = a.npatch == 1 && a.t[0] == nullptr;
   SeqMulti m;
   memset(&m, 0, sizeof(m));
   m.np = a.npatch;
   m.st = a.st;
   for (int pr = 0; pr < a.npatch; ++pr) {
-    if (!a.E[pr][d] || !a.t[pr]) return false;
+    if (!a.E[pr][d] || (!a.t[pr] && !single)) return false;
     const int bd[3] = {a.bd[pr][0], a.bd[pr][1], a.bd[pr][2]};
     const long long nbox = (long long)bd[0] * bd[1] * bd[2];
-    const long long str[3] = {a.kk, (long long)bd[0] * a.kk, (long long)bd[0] * bd[1] * a.kk};
-    const long long sc = nbox * a.kk;
+    long long str[3] = {a.kk, (long long)bd[0] * a.kk, (long long)bd[0] * bd[1] * a.kk};
+    long long sc = nbox * a.kk;
     SeqLine& tl = m.tl[pr];
     tl.t = a.t[pr]; tl.E = a.E[pr][d]; tl.n = bd[d]; tl.kk = a.kk;
+    if (single) {
+      tl.t = a.z + g.guard * a.kk;
+      str[1] = (long long)g.nx * a.kk; str[2] = (long long)g.nx * g.ny * a.kk;
+      sc = g.padded * a.kk;
+    }
     if (d == 0) {
       tl.mode = 1; tl.nlines = a.nvec * bd[1] * bd[2]; tl.nl2 = bd[1] * bd[2]; tl.sA = sc; tl.sB = str[1];
       const bool al = ((bd[0] * a.kk) & 1) == 0 && (sc & 1) == 0 &&
@@ -466,13 +475,13 @@ bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s) {
     }
   }
   switch (a.p) {
-    case 1: return seq_launch<1>(m, s);
-    case 2: return seq_launch<2>(m, s);
-    case 3: return seq_launch<3>(m, s);
-    case 4: return seq_launch<4>(m, s);
-    case 5: return seq_launch<5>(m, s);
-    case 6: return seq_launch<6>(m, s);
-    default: return seq_launch<7>(m, s);
+    case 1: return seq_launch<1>(m, s, dry);
+    case 2: return seq_launch<2>(m, s, dry);
+    case 3: return seq_launch<3>(m, s, dry);
+    case 4: return seq_launch<4>(m, s, dry);
+    case 5: return seq_launch<5>(m, s, dry);
+    case 6: return seq_launch<6>(m, s, dry);
+    default: return seq_launch<7>(m, s, dry);
   }
 }
 

@@ -688,7 +688,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
   static int line_mode = -1;  // 0 auto, 1 tile, 2 stream, 3 slab
   if (line_mode < 0) {
     const char* e = getenv("GA_LINE_MODE");
-    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : ((e && e[0] == 'b') ? 3 : 0));
+    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : ((e && e[0] == 'b') ? 3 : ((e && e[0] == 'q') ? 4 : 0)));
   }
   long long minslots = 1LL << 62;
   for (int pr = 0; pr < a.npatch; ++pr)
@@ -699,8 +699,28 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
       minslots = std::min(minslots, sl);
     }
   const bool stream = line_mode >= 2 || (line_mode == 0 && minslots >= 148LL * 128);
+  // many-line grids: whole-line sweeps from shared memory (line_seq.cu), 32 line-slots per tile:
+  // prologue pass, one launch per direction (forward + backward on-chip, every direction
+  // coalesced), epilogue pass with the dot products
+  if (single && stream && (line_mode == 4 || line_mode == 0) && a.nvec * g.npts * a.kk < (1LL << 31)) {
+    bool ok = true;
+    for (int d = 0; d < g.dim && ok; ++d) ok = launch_line_seq_multi(a, d, s, true);
+    if (ok) {
+      const long long tot = (long long)a.nvec * g.npts * a.kk;
+      k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+      for (int d = 0; d < g.dim; ++d) launch_line_seq_multi(a, d, s);
+      const unsigned int nb = red_grid((long long)a.nvec * g.npts);
+      switch (a.kk) {
+        case 1: k_prec_out<1><<<nb, NTHREADS, 0, s>>>(a); break;
+        case 2: k_prec_out<2><<<nb, NTHREADS, 0, s>>>(a); break;
+        case 3: k_prec_out<3><<<nb, NTHREADS, 0, s>>>(a); break;
+        default: k_prec_out<4><<<nb, NTHREADS, 0, s>>>(a); break;
+      }
+      return;
+    }
+  }
   // many-line 3D grids: shared-memory slab sweeps (forward + backward on-chip, coalesced x)
-  if (single && stream && line_mode != 2 && launch_precond_slab(a, s)) return;
+  if (single && stream && line_mode != 2 && line_mode != 4 && launch_precond_slab(a, s)) return;
   if (single && stream) {
     // streaming fused path (3D): first direction y (PRO, coalesced), then x, then z (EPI)
     const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};

@@ -104,7 +104,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s);
 bool launch_precond_slab(const PrecArgs& a, cudaStream_t s);
 // direction d of every patch box by the whole-line shared-memory solver (line_seq.cu); false if
 // not applicable (caller uses the chunked tiles)
-bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s);
+bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s, bool dry = false);
 int line_seq_mode();  // GA_LINE_SEQ=0: off (the chunked tiles instead)
 bool line_seq_prepare(int p);  // function attributes of degree p's kernel, outside stream capture
 

@@ -1,6 +1,7 @@
 """GPU parity of every line-solve implementation of the Kronecker preconditioner
 (P:703-713): the chunked shared-memory tiles ('t'), the streamed thread-per-line
-sweeps ('s'), the shared-memory slabs ('b') and the plane-fused y/x sweeps ('p').  The automatic choice depends
+sweeps ('s'), the shared-memory slabs ('b'), the plane-fused y/x sweeps ('p') and the whole-line
+sequential sweeps from shared memory ('q', line_seq.cu).  The automatic choice depends
 on the grid size, so each mode is forced through GA_LINE_MODE in a fresh
 process (the mode is read once per process) on small 3D cases with ragged
 slabs (free lines not a multiple of 32 slots), k = 1..3, and the elastic
@@ -49,7 +50,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["t", "s", "b", "p"])
+@pytest.mark.parametrize("mode", ["t", "s", "b", "p", "q"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}_" + "_".join(f"{k}{v}" for k, v in c[1].items()))
 def test_line_mode_parity(mode, case):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"), cfg=(case[0], case[1]))
