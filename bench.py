@@ -344,7 +344,7 @@ def run_ours(args, rank, world, local_rank):
     G = [(max(c[d] for c, _ in prob["patches"]) + 1) * (m - 1) - 1 for d in range(cfg["dim"])]
     info["npts"] = int(np.prod(G))
     kern = {}
-    names = {0: "k_spmv_sm(M)+p.q", 1: "k_spmv_sm(K)", 2: "preconditioner (k_line_tile x d, fused scaling/update/dots)",
+    names = {0: "k_spmv_sm(M)+p.q", 1: "k_spmv_sm(K)", 2: "preconditioner (Kronecker line solves x d, scaling, PCG update, dots)",
              3: "k_stage(predictor pass)", 5: "k_p_update"}
     persistent = ctx.persistent()
     mfree = ctx.matrix_free()

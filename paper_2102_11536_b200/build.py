@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgenalpha.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["genalpha.cu", "ops.cu", "slab.cu", "line_seq.cu", "spectral.cu", "spmv.cu", "spmv_sym.cu", "persist.cu"] + [f"persist_p{p}.cu" for p in range(1, 8)] + ["matfree.cu", "matfree_mp.cu"] + [f"matfree_p{p}.cu" for p in range(1, 8)] + ["assembly.cu", "host_math.cpp", "dist.cu", "partition.cpp"]
+SOURCES = ["genalpha.cu", "ops.cu", "line_seq.cu", "spectral.cu", "spmv.cu", "spmv_sym.cu", "persist.cu"] + [f"persist_p{p}.cu" for p in range(1, 8)] + ["matfree.cu", "matfree_mp.cu"] + [f"matfree_p{p}.cu" for p in range(1, 8)] + ["assembly.cu", "host_math.cpp", "dist.cu", "partition.cpp"]
 
 
 def _newest_source_mtime() -> float:

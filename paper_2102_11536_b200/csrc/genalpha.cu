@@ -353,7 +353,10 @@ int op_auto(const ga_desc* d) {
   if (d->dim == 3 && d->ncomp == 1 && d->npatch == 1) {
     const int nx = d->n + d->p - 2, nseg = (nx + 31) / 32;
     const double sym = 2.0 * 8.0 * ((S + 1) / 2) * 32.0 * nseg * (double)nx * nx;  // M + K, segment layout
-    if (sym <= 165e9 && (d->p >= 4 || nx >= 0.9 * 32 * nseg)) return 3;
+    // small grids stay on full stencils: the persistent cooperative solver (latency-bound regime,
+    // the rule of ga_create) is faster there than any graph of separate kernels
+    const bool small = nsp * d->k <= 600000.0 && S * nsp * 8.0 <= 64e6;
+    if (!small && sym <= 165e9 && (d->p >= 4 || nx >= 0.9 * 32 * nseg)) return 3;
     if (full <= 150e9) return 1;
     if (sym <= 165e9) return 3;
     return 2;
@@ -544,7 +547,7 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
     a.mf = 1; a.mfstiff = which; a.mfn = c->n; a.mfj0 = 0;
     a.mfW = which == 0 ? c->mfWM : c->mfWK; a.mfws = c->mfws;
     a.mfv = c->mftv; a.mfd = c->mftd;
-    if (which == 0 && !getenv("GA_MF_TILE")) { a.mpT1 = c->mpT1; a.mpT2 = c->mpT2; a.mpT3 = c->mpT3; }
+    if (which == 0) { a.mpT1 = c->mpT1; a.mpT2 = c->mpT2; a.mpT3 = c->mpT3; }
   }
   a.mode = mode;
   // p = z + beta p as a separate elementwise pass (measured faster than forming

@@ -658,37 +658,16 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
   }
 }
 
-bool launch_xslab(const PrecArgs& a, cudaStream_t s);  // slab.cu
-
-// The z sweep of the streamed path with the PCG epilogue (after the plane-fused y/x sweeps).
-bool launch_line_sf_epi_z(const PrecArgs& a, cudaStream_t s) {
-  const GridDesc& g = a.g;
-  const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
-  const long long str[3] = {a.kk, (long long)g.nx * a.kk, (long long)g.nx * g.ny * a.kk};
-  const long long off = g.guard * a.kk;
-  LineArgs la;
-  memset(&la, 0, sizeof(la));
-  la.t = a.z + off; la.L = a.L[0][2]; la.len = bd[2]; la.es = str[2]; la.kk = a.kk; la.nvec = a.nvec;
-  la.sc = g.padded * a.kk;
-  la.na = bd[0]; la.sa = str[0];
-  la.nb = bd[1]; la.sb = str[1];
-  la.s = a.s[0];
-  la.x = a.x + off; la.r = a.r + off; la.p = a.p0 + off; la.q = a.q + off;
-  la.pcg = a.pcg; la.st = a.st; la.partial = a.partial; la.counter = a.counter;
-  la.maxit = a.maxit; la.update = a.update; la.cond = a.cond;
-  line_sf_dispatch(a.p, la, false, true, s);
-  return true;
-}
-
 void launch_precond(const PrecArgs& a, cudaStream_t s) {
   const GridDesc& g = a.g;
   const bool single = (a.npatch == 1 && a.t[0] == nullptr);
-  // line mode: tiles (chunked, shared memory; needed when lines are few, 2D)
-  // or streaming thread-per-line sweeps (many lines, 3D).  GA_LINE_MODE overrides.
-  static int line_mode = -1;  // 0 auto, 1 tile, 2 stream, 3 slab
+  // line mode: tiles (chunked, shared memory; few lines, small grids), whole-line sweeps from
+  // shared memory (many lines; line_seq.cu) or streaming thread-per-line sweeps (fallback for
+  // lines too long for shared memory).  GA_LINE_MODE overrides.
+  static int line_mode = -1;  // 0 auto, 1 tile, 2 stream, 4 whole-line
   if (line_mode < 0) {
     const char* e = getenv("GA_LINE_MODE");
-    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : ((e && e[0] == 'b') ? 3 : ((e && e[0] == 'q') ? 4 : 0)));
+    line_mode = (e && e[0] == 't') ? 1 : ((e && e[0] == 's') ? 2 : ((e && e[0] == 'q') ? 4 : 0));
   }
   long long minslots = 1LL << 62;
   for (int pr = 0; pr < a.npatch; ++pr)
@@ -719,8 +698,6 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
       return;
     }
   }
-  // many-line 3D grids: shared-memory slab sweeps (forward + backward on-chip, coalesced x)
-  if (single && stream && line_mode != 2 && line_mode != 4 && launch_precond_slab(a, s)) return;
   if (single && stream) {
     // streaming fused path (3D): first direction y (PRO, coalesced), then x, then z (EPI)
     const int bd[3] = {a.bd[0][0], a.bd[0][1], a.bd[0][2]};
@@ -728,11 +705,8 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     const long long off = g.guard * a.kk;
     int order[3] = {1, 0, 2};
     if (g.dim == 2) { order[0] = 1; order[1] = 0; }
-    static int xslab = -1;  // GA_XSLAB=1: the middle (x) sweep as a shared-memory slab (coalesced x lines)
-    if (xslab < 0) { const char* e = getenv("GA_XSLAB"); xslab = (e && *e == '1') ? 1 : 0; }
     for (int k = 0; k < g.dim; ++k) {
       const int d = order[k];
-      if (xslab && d == 0 && g.dim == 3 && k != 0 && k != g.dim - 1 && launch_xslab(a, s)) continue;
       LineArgs la;
       memset(&la, 0, sizeof(la));
       la.t = a.z + off; la.L = a.L[0][d]; la.len = bd[d]; la.es = str[d]; la.kk = a.kk; la.nvec = a.nvec;

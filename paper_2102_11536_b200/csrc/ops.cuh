@@ -99,9 +99,6 @@ struct PrecArgs {
   double* xsum;
 };
 void launch_precond(const PrecArgs& a, cudaStream_t s);
-// 3D single patch: the three direction sweeps as shared-memory slabs (slab.cu); false if a
-// line set does not fit in shared memory (caller falls back to the streamed sweeps)
-bool launch_precond_slab(const PrecArgs& a, cudaStream_t s);
 // direction d of every patch box by the whole-line shared-memory solver (line_seq.cu); false if
 // not applicable (caller uses the chunked tiles)
 bool launch_line_seq_multi(const PrecArgs& a, int d, cudaStream_t s, bool dry = false);

@@ -189,18 +189,28 @@ class Context:
     """Owns the torch-allocated workspace of one ga_ctx.  All vectors are
     torch float64 CUDA tensors of length n_free (free-DoF order)."""
 
-    def __init__(self, desc, device="cuda", scratch_bytes=None, stream=None):
+    def __init__(self, desc, device="cuda", scratch_bytes=None, stream=None, guard_bytes=0):
+        """guard_bytes > 0: the workspace handed to ga_create sits between two guard regions of
+        that many bytes filled with a canary pattern (guards_intact() checks them: the memory
+        checks of tests/test_gpu_guards.py; compute-sanitizer is not available on the GPU pool)."""
         import torch
         self.torch = torch
         self.desc = desc
         self.n_free, ws, sc, smin = ga_query(desc)
         if scratch_bytes is not None:
             sc = max(smin, scratch_bytes)
-        self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=device)
+        g = (int(guard_bytes) + 255) // 256 * 256
+        self._guard = g
+        self._ws_bytes = ws
+        self.workspace = torch.empty(ws + 512 + 2 * g, dtype=torch.uint8, device=device)
+        if g:
+            self.workspace.fill_(0xA5)
+        base = _aligned(self.workspace).value + g
+        self._ws_off = base - self.workspace.data_ptr()
         scratch = torch.empty(sc + 256, dtype=torch.uint8, device=device)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         ctx = c_void_p()
-        code = lib.ga_create(byref(desc), _aligned(self.workspace), ws, _aligned(scratch), sc,
+        code = lib.ga_create(byref(desc), c_void_p(base), ws, _aligned(scratch), sc,
                              c_void_p(self.stream.cuda_stream), byref(ctx))
         del scratch
         if code != GA_OK:
@@ -210,6 +220,14 @@ class Context:
 
     def _s(self):
         return c_void_p(self.stream.cuda_stream)
+
+    def guards_intact(self):
+        """True if no byte of the guard regions around the workspace was overwritten."""
+        self.torch.cuda.synchronize()
+        w = self.workspace
+        lo = w[:self._ws_off]
+        hi = w[self._ws_off + (self._ws_bytes + 255) // 256 * 256:]
+        return bool((lo == 0xA5).all().item()) and bool((hi == 0xA5).all().item())
 
     def close(self):
         if getattr(self, "ctx", None):

@@ -1,10 +1,9 @@
 """GPU parity of every line-solve implementation of the Kronecker preconditioner
 (P:703-713): the chunked shared-memory tiles ('t'), the streamed thread-per-line
-sweeps ('s'), the shared-memory slabs ('b'), the plane-fused y/x sweeps ('p') and the whole-line
-sequential sweeps from shared memory ('q', line_seq.cu).  The automatic choice depends
+sweeps ('s') and the whole-line sequential sweeps from shared memory ('q', line_seq.cu).  The automatic choice depends
 on the grid size, so each mode is forced through GA_LINE_MODE in a fresh
 process (the mode is read once per process) on small 3D cases with ragged
-slabs (free lines not a multiple of 32 slots), k = 1..3, and the elastic
+tiles (free lines not a multiple of 32 slots), k = 1..3, and the elastic
 (3-component) layout; calM^{-1} is compared with the oracle element by element
 and a short trajectory in the relative M-norm."""
 import json
@@ -43,19 +42,18 @@ print(json.dumps(dict(pre=pre, errs=errs, floor=floor, status=st.status)))
 """
 
 CASES = [
-    ("c3", dict(p=3, n=7, k=2)),           # 8 free per direction: x slabs of 16 lines, ragged rows
-    ("c3", dict(p=2, n=11, k=3, rho=1.0)),  # 11 free, 3 rhs (30-slot x slabs)
+    ("c3", dict(p=3, n=7, k=2)),           # 8 free per direction: ragged tiles
+    ("c3", dict(p=2, n=11, k=3, rho=1.0)),  # 11 free, 3 rhs (10 x lines = 30 slots per tile)
     ("c3", dict(p=4, n=5, k=1)),
     ("c4", dict(p=2, n=4)),                 # elastic: 3 components
 ]
 
 
-@pytest.mark.parametrize("mode", ["t", "s", "b", "p", "q"])
+@pytest.mark.parametrize("mode", ["t", "s", "q"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}_" + "_".join(f"{k}{v}" for k, v in c[1].items()))
 def test_line_mode_parity(mode, case):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"), cfg=(case[0], case[1]))
-    # 'b': shared-memory slabs (plane fusion off); 'p': plane-fused y/x sweeps + streamed z
-    env = dict(os.environ, GA_LINE_MODE="b" if mode == "p" else mode, GA_PLANE="1" if mode == "p" else "0")
+    env = dict(os.environ, GA_LINE_MODE=mode)
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     r = json.loads(out.stdout.strip().splitlines()[-1])

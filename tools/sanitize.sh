@@ -7,7 +7,7 @@ for tool in memcheck racecheck synccheck; do
     timeout $TO $CS --tool $tool --error-exitcode 9 --print-limit 20 python tools/sanitize_cases.py $c > gpurun_out/sanitize/${tool}_${c}.log 2>&1
     echo "$tool $c rc=$?"
   done
-  for lm in t s b; do
+  for lm in t s q; do
     GA_LINE_MODE=$lm timeout $TO $CS --tool $tool --error-exitcode 9 --print-limit 20 python tools/sanitize_cases.py c3_full > gpurun_out/sanitize/${tool}_c3_line${lm}.log 2>&1
     echo "$tool c3_full GA_LINE_MODE=$lm rc=$?"
   done
