@@ -35,30 +35,80 @@ static unsigned int red_grid(long long n) {
 // ---------------------------------------------------------------------------
 // x += alpha p, r -= alpha q (when a PCG iteration precedes), then the scaled
 // input t = s o r of the (single) patch into z, or of every patch into its box.
+// the KK right-hand-side values of one grid point (contiguous, 8 KK-byte aligned): 16-byte
+// accesses for even KK
+template <int KK>
+__device__ __forceinline__ void ld_k(const double* __restrict__ p, double (&v)[KK]) {
+  if constexpr (KK % 2 == 0) {
+#pragma unroll
+    for (int h = 0; h < KK / 2; ++h) {
+      const double2 t = reinterpret_cast<const double2*>(p)[h];
+      v[2 * h] = t.x;
+      v[2 * h + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KK; ++j) v[j] = p[j];
+  }
+}
+template <int KK>
+__device__ __forceinline__ void st_k(double* __restrict__ p, const double (&v)[KK]) {
+  if constexpr (KK % 2 == 0) {
+#pragma unroll
+    for (int h = 0; h < KK / 2; ++h) reinterpret_cast<double2*>(p)[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < KK; ++j) p[j] = v[j];
+  }
+}
+
+template <int KK>
 __global__ void __launch_bounds__(NTHREADS) k_xr_prec_in(PrecArgs a) {
   if (a.st->status != 0) return;
   count_launch(a.st);
   const GridDesc g = a.g;
-  const long long tot = (long long)a.nvec * g.npts * a.kk;
+  const long long tot = (long long)a.nvec * g.npts;  // one thread per (component, grid point)
   const long long e = (long long)gtid();
   if (e >= tot) return;
-  const int j = (int)(e % a.kk);
-  const long long ci = e / a.kk;
-  const long long i = ci % g.npts;
-  const int c = (int)(ci / g.npts);
-  const long long idx = ((long long)c * g.padded + g.guard + i) * a.kk + j;
-  double r = a.r[idx];
+  const long long i = e % g.npts;
+  const int c = (int)(e / g.npts);
+  const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+  double r[KK];
+  ld_k<KK>(a.r + base, r);
   if (a.update && !a.pcg->first) {
-    const double al = a.pcg->alpha[j];
     const double* pp = (a.pcg->iter & 1) ? a.p1 : a.p0;
-    if (al != 0.0) {
-      a.x[idx] = fma(al, pp[idx], a.x[idx]);
-      r = fma(-al, a.q[idx], r);
-      a.r[idx] = r;
+    double al[KK];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) { al[j] = a.pcg->alpha[j]; any |= al[j] != 0.0; }
+    if (any) {
+      double x[KK], p[KK], q[KK];
+      ld_k<KK>(a.x + base, x);
+      ld_k<KK>(pp + base, p);
+      ld_k<KK>(a.q + base, q);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {  // alpha_j = 0 (converged block): x, r unchanged bit for bit
+        if (al[j] != 0.0) { x[j] = fma(al[j], p[j], x[j]); r[j] = fma(-al[j], q[j], r[j]); }
+      }
+      st_k<KK>(a.x + base, x);
+      st_k<KK>(a.r + base, r);
     }
   }
   if (a.npatch == 1 && a.t[0] == nullptr) {
-    a.z[idx] = a.s[0][i] * r;
+    const double sv = a.s[0][i];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) r[j] *= sv;
+    st_k<KK>(a.z + base, r);
+  }
+}
+static void launch_xr_prec_in(const PrecArgs& a, cudaStream_t s) {
+  const long long tot = (long long)a.nvec * a.g.npts;
+  const unsigned int nb = (unsigned int)((tot + NTHREADS - 1) / NTHREADS);
+  switch (a.kk) {
+    case 1: k_xr_prec_in<1><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 2: k_xr_prec_in<2><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 3: k_xr_prec_in<3><<<nb, NTHREADS, 0, s>>>(a); break;
+    default: k_xr_prec_in<4><<<nb, NTHREADS, 0, s>>>(a); break;
   }
 }
 
@@ -71,21 +121,29 @@ __global__ void __launch_bounds__(NTHREADS) k_xr_gather(PrecArgs a) {
   count_launch(a.st);
   const GridDesc g = a.g;
   const int npts = (int)g.npts;
-  const int tot = a.nvec * npts * KK;
+  const int tot = a.nvec * npts;  // one thread per (component, grid point): 16-byte accesses for even KK
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= tot) return;
-  const int j = e % KK;
-  const int ci = e / KK;
-  const int c = ci / npts, i = ci - c * npts;
-  const long long idx = ((long long)c * g.padded + g.guard + i) * KK + j;
-  double r = a.r[idx];
+  const int c = e / npts, i = e - c * npts;
+  const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+  double r[KK];
+  ld_k<KK>(a.r + base, r);
   if (a.update && !a.pcg->first) {
-    const double al = a.pcg->alpha[j];
     const double* pp = (a.pcg->iter & 1) ? a.p1 : a.p0;
-    if (al != 0.0) {
-      a.x[idx] = fma(al, pp[idx], a.x[idx]);
-      r = fma(-al, a.q[idx], r);
-      a.r[idx] = r;
+    double al[KK];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) { al[j] = a.pcg->alpha[j]; any |= al[j] != 0.0; }
+    if (any) {
+      double x[KK], p[KK], q[KK];
+      ld_k<KK>(a.x + base, x);
+      ld_k<KK>(pp + base, p);
+      ld_k<KK>(a.q + base, q);
+#pragma unroll
+      for (int j = 0; j < KK; ++j)
+        if (al[j] != 0.0) { x[j] = fma(al[j], p[j], x[j]); r[j] = fma(-al[j], q[j], r[j]); }
+      st_k<KK>(a.x + base, x);
+      st_k<KK>(a.r + base, r);
     }
   }
   const int ix = i % g.nx, iyz = i / g.nx;
@@ -96,7 +154,11 @@ __global__ void __launch_bounds__(NTHREADS) k_xr_gather(PrecArgs a) {
     if (lx < 0 || ly < 0 || lz < 0 || lx >= bx || ly >= by || lz >= bz) continue;
     const int bi = lx + bx * (ly + by * lz);
     const long long nbox = (long long)bx * by * bz;
-    a.t[pr][((long long)c * nbox + bi) * KK + j] = a.s[pr][bi] * r;
+    const double sv = a.s[pr][bi];
+    double t[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) t[j] = sv * r[j];
+    st_k<KK>(a.t[pr] + ((long long)c * nbox + bi) * KK, t);
   }
 }
 
@@ -614,8 +676,9 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
     double z[KK];
     if (a.npatch == 1 && a.t[0] == nullptr) {
       const double sv = a.s[0][i];
+      ld_k<KK>(a.z + base, z);
 #pragma unroll
-      for (int j = 0; j < KK; ++j) z[j] = sv * a.z[base + j];
+      for (int j = 0; j < KK; ++j) z[j] *= sv;
     } else {
 #pragma unroll
       for (int j = 0; j < KK; ++j) z[j] = 0.0;
@@ -637,12 +700,13 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
     // subdomain (a.xsum): r.z over every local DoF (z_r unassembled: r.z = sum_r r_r . z_r),
     // r.r over the owned DoFs only (each global DoF once)
     const double wr = (a.xsum && a.mask && a.mask[i] != 1) ? 0.0 : 1.0;
+    double rv[KK];
+    ld_k<KK>(a.r + base, rv);
+    st_k<KK>(a.z + base, z);
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
-      a.z[base + j] = z[j];
-      const double r = a.r[base + j];
-      v[j] = fma(r, z[j], v[j]);
-      v[KK + j] = fma(wr * r, r, v[KK + j]);
+      v[j] = fma(rv[j], z[j], v[j]);
+      v[KK + j] = fma(wr * rv[j], rv[j], v[KK + j]);
     }
   }
   if (dead) return;
@@ -685,8 +749,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     bool ok = true;
     for (int d = 0; d < g.dim && ok; ++d) ok = launch_line_seq_multi(a, d, s, true);
     if (ok) {
-      const long long tot = (long long)a.nvec * g.npts * a.kk;
-      k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+      launch_xr_prec_in(a, s);
       for (int d = 0; d < g.dim; ++d) launch_line_seq_multi(a, d, s);
       const unsigned int nb = red_grid((long long)a.nvec * g.npts);
       switch (a.kk) {
@@ -761,7 +824,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
   const bool batched = !single && !stream;
   if (batched && a.nvec * g.npts * a.kk < (1LL << 31)) {
     // batched Schwarz: prologue + gather in one pass, then one tile launch per direction
-    const unsigned int nbg = (unsigned int)((a.nvec * g.npts * a.kk + NTHREADS - 1) / NTHREADS);
+    const unsigned int nbg = (unsigned int)((a.nvec * g.npts + NTHREADS - 1) / NTHREADS);
     switch (a.kk) {
       case 1: k_xr_gather<1><<<nbg, NTHREADS, 0, s>>>(a); break;
       case 2: k_xr_gather<2><<<nbg, NTHREADS, 0, s>>>(a); break;
@@ -769,8 +832,7 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
       default: k_xr_gather<4><<<nbg, NTHREADS, 0, s>>>(a); break;
     }
   } else {
-    const long long tot = (long long)a.nvec * g.npts * a.kk;
-    k_xr_prec_in<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+    launch_xr_prec_in(a, s);
     if (batched) {
       long long tb = 0;
       for (int pr = 0; pr < a.npatch; ++pr) tb += (long long)a.nvec * a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2] * a.kk;
@@ -929,25 +991,39 @@ void launch_init_from_b(const VecArgs& a, cudaStream_t s) {
 }
 
 // p = z (first iteration of a phase) or p = z + beta p, for active blocks.
+template <int KK>
 __global__ void __launch_bounds__(NTHREADS) k_p_update(VecArgs a) {
   if (a.st->status != 0) return;
   count_launch(a.st);
   const GridDesc g = a.g;
-  const long long tot = (long long)a.nvec * g.npts * a.kk;
+  const long long tot = (long long)a.nvec * g.npts;  // one thread per (component, grid point)
   const long long e = (long long)gtid();
   if (e >= tot) return;
-  const int j = (int)(e % a.kk);
-  if (!a.pcg->active[j]) return;
-  const long long ci = e / a.kk;
-  const long long i = ci % g.npts;
-  const int c = (int)(ci / g.npts);
-  const long long idx = ((long long)c * g.padded + g.guard + i) * a.kk + j;
-  const double z = a.z[idx];
-  a.p[idx] = a.pcg->pfirst ? z : fma(a.pcg->beta[j], a.p[idx], z);
+  const long long i = e % g.npts;
+  const int c = (int)(e / g.npts);
+  const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < KK; ++j) any |= a.pcg->active[j] != 0;
+  if (!any) return;
+  double z[KK], p[KK];
+  ld_k<KK>(a.z + base, z);
+  ld_k<KK>(a.p + base, p);
+  const bool pfirst = a.pcg->pfirst != 0;
+#pragma unroll
+  for (int j = 0; j < KK; ++j)
+    if (a.pcg->active[j]) p[j] = pfirst ? z[j] : fma(a.pcg->beta[j], p[j], z[j]);  // inactive: unchanged
+  st_k<KK>(a.p + base, p);
 }
 void launch_p_update(const VecArgs& a, cudaStream_t s) {
-  const long long tot = (long long)a.nvec * a.g.npts * a.kk;
-  k_p_update<<<(unsigned int)((tot + NTHREADS - 1) / NTHREADS), NTHREADS, 0, s>>>(a);
+  const long long tot = (long long)a.nvec * a.g.npts;
+  const unsigned int nb = (unsigned int)((tot + NTHREADS - 1) / NTHREADS);
+  switch (a.kk) {
+    case 1: k_p_update<1><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 2: k_p_update<2><<<nb, NTHREADS, 0, s>>>(a); break;
+    case 3: k_p_update<3><<<nb, NTHREADS, 0, s>>>(a); break;
+    default: k_p_update<4><<<nb, NTHREADS, 0, s>>>(a); break;
+  }
 }
 
 __global__ void k_solve_end(PcgState* pc, DevStatus* st) {
