@@ -21,7 +21,10 @@ from _helpers import Case
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("p,n,k", [(3, 100, 2), (2, 140, 1), (5, 80, 3)])
+# (p, n, k): even and odd free counts x k = 1..4 (bulk copies need 16-byte lines: odd n_f k falls back
+# to 8-byte cp.async), every batch size of the sweeps (p <= 4: 8, p >= 5: 4), p = 1 and p = 7
+@pytest.mark.parametrize("p,n,k", [(3, 100, 2), (2, 140, 1), (5, 80, 3), (2, 139, 1), (3, 81, 3), (1, 73, 4),
+                                   (4, 101, 2), (7, 94, 2), (6, 99, 1)])
 def test_kronecker_identity_on_the_cube(p, n, k):
     import torch
     from paper_2102_11536_b200 import Context, make_desc
