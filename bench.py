@@ -364,6 +364,9 @@ def run_ours(args, rank, world, local_rank):
     L = loop_iters / steps  # lock-stepped PCG iterations per step (one solve set per step)
     nsolve_phases = 2 if True else 1  # main phase + refinement restart
     info_bytes = {op: algorithmic_bytes(op, info) for op in (0, 1, 2, 3)}
+    if cfg.get("lshape"):  # masked grid: only the free rows have coefficients to read (masked row blocks are skipped)
+        for op in (0, 1):
+            info_bytes[op] = algorithmic_bytes(op, dict(info, npts=n_free // nc))
     if opmode == 3 and nc == 3:  # the elastic K stays a full 3x3-block stencil
         info_bytes[1] = algorithmic_bytes(1, dict(info, S=(2 * cfg["p"] + 1) ** cfg["dim"]))
     info_bytes[5] = 24 * info["nvec"] * info["k"] * info["npts"]

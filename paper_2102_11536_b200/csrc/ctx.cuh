@@ -55,6 +55,7 @@ struct ga_ctx {
   double *coefM = nullptr, *coefK = nullptr, *chain = nullptr;
   double *pred = nullptr, *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr, *pv1 = nullptr;
   unsigned char* mask = nullptr;
+  unsigned char* blkskip = nullptr;  // per 32-row block: 1 = no free row (masked grids), SpmvArgs::skip
   long long* map = nullptr;
   PcgState* pcg = nullptr;
   DevStatus* st = nullptr;

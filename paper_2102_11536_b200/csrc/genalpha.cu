@@ -77,7 +77,7 @@ void seterr(ga_ctx* ctx, const std::string& s) {
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t off_coefM, off_coefK, off_symzero, off_chain, off_mv[8], off_mask, off_map, off_pcg, off_st, off_partial, off_counter,
+  size_t off_coefM, off_coefK, off_symzero, off_chain, off_mv[8], off_mask, off_skip, off_map, off_pcg, off_st, off_partial, off_counter,
       off_dscal, off_mfWM, off_mfWK, off_mftab, off_diag, off_mpT1, off_mpT2, off_mpT3, off_forceG, off_fslots,
       off_lz, off_lzab, off_xgi, off_xslot, off_xinv, off_xbuf, off_xrecv;
   std::vector<size_t> off_s, off_t, off_L[3], off_F[3], off_E[3];
@@ -410,6 +410,7 @@ Layout make_layout(const Shape& sh) {
   for (int i = 0; i < 8; ++i) L.off_mv[i] = take(sizeof(double) * sh.nvec * sh.g.padded * sh.k);
   const bool multi = sh.prec.size() > 1 || sh.sub;
   L.off_mask = take(multi ? npts : 0);
+  L.off_skip = take(multi ? (npts + 31) / 32 : 0);
   L.off_map = take(multi ? sizeof(long long) * sh.nfree : 0);
   L.off_pcg = take(sizeof(PcgState));
   L.off_st = take(sizeof(DevStatus));
@@ -541,6 +542,7 @@ SpmvArgs spmv_args(ga_ctx* c, int which, const double* x, double* y, int mode) {
   a.x = x; a.y = y; a.b = c->b;
   a.g = c->g; a.nvec = c->nvec; a.kk = c->k; a.p = c->p;
   a.elastic = (which == 1 && c->nvec == 3) ? 1 : 0;
+  a.skip = c->blkskip;
   if (c->half && !a.elastic) { a.half = 1; a.hguard = c->g.guard; }
   if (c->sym && !a.elastic) { a.sym = 1; a.sxs = c->sl.xs; a.snseg = c->sl.nseg; a.symzero = c->symzero; }
   if (c->mf && !a.elastic) {
@@ -1098,6 +1100,7 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
     ctx->diagM = (double*)(ws + L.off_diag);
   }
   ctx->mask = multi ? (unsigned char*)(ws + L.off_mask) : nullptr;
+  ctx->blkskip = multi ? (unsigned char*)(ws + L.off_skip) : nullptr;
   ctx->map = multi ? (long long*)(ws + L.off_map) : nullptr;
   ctx->pcg = (PcgState*)(ws + L.off_pcg);
   ctx->st = (DevStatus*)(ws + L.off_st);
@@ -1125,6 +1128,13 @@ ga_status ga_create(const ga_desc* desc, void* d_workspace, size_t workspace_byt
   if (sh.sym) CKD(cudaMemsetAsync(ws + L.off_symzero, 0, sizeof(double) * ((sh.S + 1) / 2) * SYM_STRIDE, s));
   if (multi) {
     CKD(cudaMemcpyAsync(ctx->mask, sh.mask.data(), sh.g.npts, cudaMemcpyHostToDevice, s));
+    {
+      const long long nrb = (sh.g.npts + 31) / 32;
+      std::vector<unsigned char> skip((size_t)nrb, 1);
+      for (long long gi = 0; gi < sh.g.npts; ++gi)
+        if (sh.mask[gi]) skip[(size_t)(gi >> 5)] = 0;
+      CKD(cudaMemcpy(ctx->blkskip, skip.data(), (size_t)nrb, cudaMemcpyHostToDevice));
+    }
     CKD(cudaMemcpyAsync(ctx->map, sh.map.data(), sizeof(long long) * sh.nfree, cudaMemcpyHostToDevice, s));
   }
   std::vector<int> hxinv;

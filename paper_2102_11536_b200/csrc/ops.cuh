@@ -56,6 +56,10 @@ struct SpmvArgs {
   // subdomain group (dist.cu): SPMV_PQ writes its local p.q sums here (k_spmv_fin) instead of
   // taking the PCG scalar step, which runs after the exchange (null: ordinary context)
   double* xsum;
+  // masked grids (multi-patch): skip[rb] = 1 if none of the 32 rows of row block rb is free (its
+  // rows and columns are zero, and every vector is zero there): the warp of that block does
+  // nothing.  C5: the [1,2]^2 quadrant of the L-shape's bounding grid, 25 % of the row blocks.
+  const unsigned char* skip;
 };
 void launch_spmv(const SpmvArgs& a, cudaStream_t s);
 void launch_spmv_sym(const SpmvArgs& a, cudaStream_t s);  // a.sym = 1 (spmv_sym.cu)

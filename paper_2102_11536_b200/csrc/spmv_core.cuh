@@ -41,6 +41,7 @@ __device__ __forceinline__ void spmv_block(const SpmvArgs& a, long long rbg, dou
   const long long rb = rbg * G + gq;
   const long long i0 = rb * BR;
   if (i0 >= g.npts) return;  // whole warp
+  if (a.skip && a.skip[rb]) return;  // no free row in this block (masked grid)
   const long long i = i0 + r;
   const bool valid = i < g.npts;
   const long long icl = valid ? i : (g.npts - 1);  // clamp coefficient reads of the tail rows
@@ -187,6 +188,7 @@ __device__ __forceinline__ void spmv_block_half(const SpmvArgs& a, long long rbg
   const long long rb = rbg * G + gq;
   const long long i0 = rb * BR;
   if (i0 >= g.npts) return;
+  if (a.skip && a.skip[rb]) return;  // no free row in this block (masked grid)
   const long long i = i0 + r;
   const bool valid = i < g.npts;
   const long long icl = valid ? i : (g.npts - 1);
