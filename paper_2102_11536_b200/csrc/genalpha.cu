@@ -569,6 +569,7 @@ VecArgs vec_args(ga_ctx* c) {
   a.x = c->x; a.r = c->r; a.z = c->z; a.p = c->pv; a.b = c->b;
   a.pcg = c->pcg; a.st = c->st; a.partial = c->partial; a.counter = c->counter;
   a.own = nullptr; a.xsum = nullptr;
+  a.mask = c->mask;
   return a;
 }
 

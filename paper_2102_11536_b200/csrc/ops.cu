@@ -126,9 +126,12 @@ __global__ void __launch_bounds__(NTHREADS) k_xr_gather(PrecArgs a) {
   if (e >= tot) return;
   const int c = e / npts, i = e - c * npts;
   const long long base = ((long long)c * g.padded + g.guard + i) * KK;
+  const bool free_pt = a.mask == nullptr || a.mask[i];  // not free: r = 0, only the boxes get their zeros
   double r[KK];
-  ld_k<KK>(a.r + base, r);
-  if (a.update && !a.pcg->first) {
+#pragma unroll
+  for (int j = 0; j < KK; ++j) r[j] = 0.0;
+  if (free_pt) ld_k<KK>(a.r + base, r);
+  if (free_pt && a.update && !a.pcg->first) {
     const double* pp = (a.pcg->iter & 1) ? a.p1 : a.p0;
     double al[KK];
     bool any = false;
@@ -684,17 +687,17 @@ __global__ void __launch_bounds__(NTHREADS) k_prec_out(PrecArgs a) {
       for (int j = 0; j < KK; ++j) z[j] = 0.0;
       const int iyz = i / g.nx, ix = i - iyz * g.nx;
       const int iz = iyz / g.ny, iy = iyz - iz * g.ny;
-      const bool free_pt = a.mask == nullptr || a.mask[i];
-      if (free_pt) {
-        for (int pr = 0; pr < a.npatch; ++pr) {
-          const int lx = ix - a.lo[pr][0], ly = iy - a.lo[pr][1], lz = iz - a.lo[pr][2];
-          if (lx < 0 || ly < 0 || lz < 0 || lx >= a.bd[pr][0] || ly >= a.bd[pr][1] || lz >= a.bd[pr][2]) continue;
-          const long long nbox = (long long)a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2];
-          const int bi = lx + a.bd[pr][0] * (ly + a.bd[pr][1] * lz);
-          const double sv = a.s[pr][bi];
+      if (a.mask != nullptr && !a.mask[i]) continue;  // not free: z and r stay zero there
+      for (int pr = 0; pr < a.npatch; ++pr) {
+        const int lx = ix - a.lo[pr][0], ly = iy - a.lo[pr][1], lz = iz - a.lo[pr][2];
+        if (lx < 0 || ly < 0 || lz < 0 || lx >= a.bd[pr][0] || ly >= a.bd[pr][1] || lz >= a.bd[pr][2]) continue;
+        const long long nbox = (long long)a.bd[pr][0] * a.bd[pr][1] * a.bd[pr][2];
+        const int bi = lx + a.bd[pr][0] * (ly + a.bd[pr][1] * lz);
+        const double sv = a.s[pr][bi];
+        double tv[KK];
+        ld_k<KK>(a.t[pr] + ((long long)c * nbox + bi) * KK, tv);
 #pragma unroll
-          for (int j = 0; j < KK; ++j) z[j] = fma(sv, a.t[pr][((long long)c * nbox + bi) * KK + j], z[j]);
-        }
+        for (int j = 0; j < KK; ++j) z[j] = fma(sv, tv[j], z[j]);
       }
     }
     // subdomain (a.xsum): r.z over every local DoF (z_r unassembled: r.z = sum_r r_r . z_r),
@@ -1001,6 +1004,7 @@ __global__ void __launch_bounds__(NTHREADS) k_p_update(VecArgs a) {
   if (e >= tot) return;
   const long long i = e % g.npts;
   const int c = (int)(e / g.npts);
+  if (a.mask && !a.mask[i]) return;  // not a free point: every vector is zero there
   const long long base = ((long long)c * g.padded + g.guard + i) * KK;
   bool any = false;
 #pragma unroll

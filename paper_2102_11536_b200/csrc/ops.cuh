@@ -122,6 +122,7 @@ struct VecArgs {
   // leaves the PcgState set-up to the step after the exchange; null: ordinary context
   const unsigned char* own;
   double* xsum;
+  const unsigned char* mask;  // grid mask (masked grids: points that are not free are skipped), or null
 };
 void launch_init_from_b(const VecArgs& a, cudaStream_t s);
 void launch_p_update(const VecArgs& a, cudaStream_t s);
