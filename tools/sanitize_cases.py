@@ -1,7 +1,7 @@
 """Small invocations of every hot-path kernel family for compute-sanitizer (memcheck, racecheck,
 synccheck): persistent cooperative solver (C1, C2 reduced), graph PCG with the 2D tile line
 solves, the multi-patch Schwarz path (C5 reduced), the 3D line-solve modes (tiles / streamed /
-slabs, forced by GA_LINE_MODE in separate processes), the single-read symmetric SpMV (3D
+whole-line, forced by GA_LINE_MODE in separate processes), the single-read symmetric SpMV (3D
 half-symmetric), the elastic row tiles and the matrix-free operators.  Usage:
   compute-sanitizer --tool memcheck python tools/sanitize_cases.py <case>"""
 import math
