@@ -407,7 +407,7 @@ static bool seq_launch(SeqMulti m, cudaStream_t s, bool dry) {
     for (int r = 0; r < m.np; ++r) ct += tiles(m.tl[r], cand);
     const long long per_sm = std::min<long long>(16, (long long)(227 * 1024) / (long long)(sm + 1024 + (227 * 1024 - dyn_max)));
     TS = cand;
-    if (ct <= std::min<long long>(per_sm, 4) * nsm) break;  // one sweep warp per scheduler
+    if (ct <= std::min<long long>(per_sm, 4) * nsm) break;  // <= 4 sweep warps per SM (measured: 3 are free)
   }
   if (!TS) return false;
   for (int r = 0; r < m.np; ++r)
