@@ -335,8 +335,10 @@ __global__ void __launch_bounds__(NTHREADS) k_sym_dots(SpmvArgs a) {
   }
 }
 
+// plan only (eff_out != nullptr): the modelled efficiency of this TY with its best chunk count,
+// no launch
 template <int P, int KK, int TY, int D>
-static bool launch_sym_ty(const SpmvArgs& a, cudaStream_t s) {
+static bool launch_sym_ty(const SpmvArgs& a, cudaStream_t s, double* eff_out = nullptr) {
   using SS = SymShape<P, KK, TY, D>;
   if constexpr (SS::bytes > 225 * 1024) {
     return false;
@@ -373,6 +375,7 @@ static bool launch_sym_ty(const SpmvArgs& a, cudaStream_t s) {
       const double eff = ctas / (waves * slots) * (double)zl / (zl + 0.5 * P);
       if (eff > best + 1e-9) { best = eff; nch = cc; }
     }
+    if (eff_out) { *eff_out = best * (double)g.ny / ((double)nty * TY); return true; }
     if (force_nch > 0) nch = std::min<long long>(force_nch, g.nz);
     const int zlen = (int)((g.nz + nch - 1) / nch);
     nch = (g.nz + zlen - 1) / zlen;
@@ -388,15 +391,26 @@ static bool launch_sym_ty(const SpmvArgs& a, cudaStream_t s) {
   }
 }
 
-// warps (y-lines) per CTA: TY = 4 (two CTAs per SM); GA_SYM_TY = 2 / 4 / 8 overrides (measurement)
+// warps (y-lines) per CTA: TY = 4 (two CTAs per SM) unless 2-warp CTAs fill the resident slots
+// clearly better in whole waves (modelled efficiency of launch_sym_ty; measured: C3 p=4 n=96
+// 747 -> 616 us per M apply with TY = 2, equal at p=4 n=192, TY = 4 3 % faster at p=2 n=192);
+// GA_SYM_TY = 2 / 4 / 8 overrides (measurement)
 template <int P, int KK>
 static void launch_sym_kk(const SpmvArgs& a, cudaStream_t s) {
   static int ty = -1;
   if (ty < 0) {
     const char* e = getenv("GA_SYM_TY");
-    ty = e ? atoi(e) : 4;
+    ty = e ? atoi(e) : 0;
   }
   constexpr int D = (2 * P + 1) < 4 ? (2 * P + 1) : 4;  // prefetched rows (at most one stage ahead)
+  if (ty == 0) {
+    double e4 = 0.0, e2 = 0.0;
+    const bool ok4 = launch_sym_ty<P, KK, 4, D>(a, s, &e4);
+    const bool ok2 = launch_sym_ty<P, KK, 2, D>(a, s, &e2);
+    if (ok4 && !(ok2 && e2 > 1.08 * e4)) { launch_sym_ty<P, KK, 4, D>(a, s); return; }
+    launch_sym_ty<P, KK, 2, D>(a, s);
+    return;
+  }
   if (ty >= 8 && launch_sym_ty<P, KK, 8, D>(a, s)) return;
   if (ty >= 4 && launch_sym_ty<P, KK, 4, D>(a, s)) return;
   launch_sym_ty<P, KK, 2, D>(a, s);
