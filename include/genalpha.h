@@ -122,10 +122,15 @@ typedef struct {
                         /* 1: assembled column-index-free stencils (2p+1)^dim per row;  */
                         /* 2: matrix-free sum factorisation from the Gauss-point data   */
                         /*    (single patch only; the elastic K stays a stencil);       */
-                        /* 3: half-symmetric stencils, offsets o >= 0 only (same bytes  */
-                        /*    per apply, half the memory; the elastic K stays full);    */
-                        /* 0: auto = full stencils if they fit in ~150 GB, else half-   */
-                        /*    symmetric, else matrix-free (measured, R14)     */
+                        /* 3: half-symmetric stencils, offsets o >= 0 only: half the    */
+                        /*    memory; 3D scalar grids read each stored coefficient once */
+                        /*    (single-read symmetric SpMV, half the bytes per apply),   */
+                        /*    2D and the elastic mass twice; the elastic K stays full;  */
+                        /* 0: auto, the measured-faster one (R14): 3D scalar  */
+                        /*    grids beyond the persistent solver's size take 3 when     */
+                        /*    p >= 3 or the 32-point x-segments are >= 90 % used; else  */
+                        /*    full stencils if they fit in ~150 GB, else half-          */
+                        /*    symmetric, else matrix-free                               */
   double damp_a0, damp_a1; /* Rayleigh damping C = damp_a0 M + damp_a1 K, >= 0 (SURVEY    */
                         /* NEXT-2; reading R16: block j subtracts C w_j, w_j the Taylor */
                         /* predictor of its velocity-level entry for j < k); 0 0: none  */
