@@ -128,7 +128,7 @@ typedef struct {
                         /*    2D and the elastic mass twice; the elastic K stays full;  */
                         /* 0: auto, the measured-faster one (R14): 3D scalar  */
                         /*    grids beyond the persistent solver's size take 3 when     */
-                        /*    p >= 3 or the 32-point x-segments are >= 90 % used; else  */
+                        /*    p >= 4, or the 32-point x-segments are well used; else    */
                         /*    full stencils if they fit in ~150 GB, else half-          */
                         /*    symmetric, else matrix-free                               */
   double damp_a0, damp_a1; /* Rayleigh damping C = damp_a0 M + damp_a1 K, >= 0 (SURVEY    */

@@ -358,7 +358,9 @@ int op_auto(const ga_desc* d) {
     const bool small = nsp * d->k <= 600000.0 && S * nsp * 8.0 <= 64e6;
     // measured (tools/kbench.py, step time, sym vs full): p=3 n=96/128/160/192 6.99/12.6/22.6/38.3 vs
     // 7.52/14.5/28.8/49.4 ms; p=2 n=100 (78 % of the x-segments used) 3.45 vs 3.31 ms
-    if (!small && sym <= 165e9 && (d->p >= 3 || nx >= 0.9 * 32 * nseg)) return 3;
+    // p=3 n=64 (68 % used): 3.18 vs 2.82 ms; p >= 4: symmetric at every measured size (n = 48..192)
+    const double need = d->p >= 4 ? 0.0 : (d->p == 3 ? 0.72 : 0.9);
+    if (!small && sym <= 165e9 && nx >= need * 32 * nseg) return 3;
     if (full <= 150e9) return 1;
     if (sym <= 165e9) return 3;
     return 2;
