@@ -745,10 +745,18 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
       minslots = std::min(minslots, sl);
     }
   const bool stream = line_mode >= 2 || (line_mode == 0 && minslots >= 148LL * 128);
-  // many-line grids: whole-line sweeps from shared memory (line_seq.cu), 32 line-slots per tile:
-  // prologue pass, one launch per direction (forward + backward on-chip, every direction
-  // coalesced), epilogue pass with the dot products
-  if (single && stream && (line_mode == 4 || line_mode == 0) && a.nvec * g.npts * a.kk < (1LL << 31)) {
+  // single patch: whole-line sweeps from shared memory (line_seq.cu): prologue pass, one launch per
+  // direction (forward + backward on-chip, every direction coalesced), epilogue pass with the dot
+  // products.  Auto: every 3D grid (measured against the fused chunked tiles, step times: n_f = 27
+  // 4.39 vs 4.74 ms, 34: 2.11 vs 2.04, 49: 1.49 vs 1.93, 66: 5.07 vs 6.09, 81: 3.77 vs 4.45 ms) and
+  // 2D grids with lines longer than 768 points (2D p=3 n=512: 1.28 vs 1.19 ms for the tiles;
+  // n=1024: 2.8 vs 16.7 ms, n=2048: 18.5 vs 38.5 ms - the tiles' 64-chunk limit)
+  bool want_seq = line_mode == 4;
+  if (line_mode == 0 && single) {
+    const int lmax = std::max(a.bd[0][0], std::max(a.bd[0][1], a.bd[0][2]));
+    want_seq = g.dim == 3 || lmax > 768 || stream;
+  }
+  if (single && want_seq && a.nvec * g.npts * a.kk < (1LL << 31)) {
     bool ok = true;
     for (int d = 0; d < g.dim && ok; ++d) ok = launch_line_seq_multi(a, d, s, true);
     if (ok) {
