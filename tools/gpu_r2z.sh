@@ -1,4 +1,6 @@
-out=gpurun_out/r2z_configs.jsonl; : > $out
-run() { timeout 1200 python bench.py "$@" --no-cpu-baseline --kernel-reps 3 >> $out 2>> gpurun_out/r2z_err.txt || echo "{\"failed\": \"$*\"}" >> $out; }
-run --config c3 --p 6 --n 48 --steps 10 --warmup 3
-python tools/configs_table.py $out | cut -c1-60,150-330
+for ts in 4 16 32; do
+echo "== c5 GA_SEQ_MINTS=$ts"; GA_SEQ_MINTS=$ts python tools/kbench.py c5 reps=20 2>&1 | grep -E "precond|step"
+done
+for ts in 4 16; do
+echo "== c3 p=4 n=48 GA_SEQ_MINTS=$ts"; GA_SEQ_MINTS=$ts python tools/kbench.py c3 p=4 n=48 reps=20 2>&1 | grep -E "precond|step"
+done
