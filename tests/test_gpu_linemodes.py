@@ -46,6 +46,8 @@ CASES = [
     ("c3", dict(p=2, n=11, k=3, rho=1.0)),  # 11 free, 3 rhs (10 x lines = 30 slots per tile)
     ("c3", dict(p=4, n=5, k=1)),
     ("c4", dict(p=2, n=4)),                 # elastic: 3 components
+    ("c3", dict(p=5, n=4, k=2)),            # p >= 5: batches of 4 in the whole-line sweeps, 64-byte factor rows
+    ("c3", dict(p=1, n=9, k=4)),            # p = 1, 4 right-hand sides
 ]
 
 
