@@ -1,18 +1,22 @@
-// Whole-line sequential Kronecker line solves from shared memory (DESIGN.md "Line solves, few long
-// lines"): the factor Mh_d^{-1} of calM^{-1} for grids with few, long lines (2D:
-// C2 257 lines, C5 514 per patch), where a thread-per-line recurrence is latency-bound and the
-// chunked tiles (tile_core.cuh) pay a scan of ~50 chunk states per sweep.
+// Whole-line sequential Kronecker line solves from shared memory (DESIGN.md §6 "Whole-line
+// solver"): the factor Mh_d^{-1} of calM^{-1}.  Used for the boxes of a
+// multi-patch problem (additive Schwarz, C5: 514 lines x 2 right-hand sides per patch and
+// direction, where a thread-per-line recurrence is latency-bound and the chunked tiles of
+// tile_core.cuh pay a scan of ~50 chunk states per sweep), for every 3D single-patch grid outside
+// the persistent solver and for 2D grids with lines longer than 768 points.
 //
 // A CTA of 4 warps stages TS line-slots (a line x one right-hand side) over the WHOLE line length
-// in shared memory, together with the two sweeps' factor rows; then ONE warp, one lane per slot,
-// runs the banded forward and backward substitutions straight through the line (the sweep is
-// bound by instruction issue per warp and by the recurrence, not by lanes: fewer, fuller warps).  The divisions are folded
-// into the band on the host (host_math.cpp make_seq): y_i = t_i d_i - sum_u e_{i,u} y_{i-u}, and the
-// term of y_{i-1} is taken last, so ONE fp64 FMA per element is on the recurrence's critical path;
-// data and factor rows of the next batch of elements are loaded into registers while the current
-// batch is computed (the loads do not depend on the recurrence).  TS is chosen as small as possible
-// with all tiles of a sweep resident at once and at most one sweep warp per SM scheduler (C5: 387
-// CTAs of 8 slots, 2-3 per SM, their sweep warps on different schedulers by arrival order).
+// in shared memory, together with the two sweeps' factor rows; then ONE warp (warp 0), one lane per
+// slot, runs the banded forward and backward substitutions straight through the line - the sweep
+// is bound by the instruction stream per warp and by the recurrence, not by lanes, so fewer,
+// fuller warps win.  The divisions are folded into the band on the host (host_math.cpp make_seq):
+// y_i = t_i d_i - sum_u e_{i,u} y_{i-u}, and the term of y_{i-1} is taken last, so ONE fp64 FMA per
+// element is on the recurrence's critical path; data and factor rows of the next batch of elements
+// are loaded into registers while the current batch is computed (the loads do not depend on the
+// recurrence).  TS is the smallest power of two in 4..32 with all tiles of the launch resident at
+// once and at most 4 sweep warps per SM (C5: 387 CTAs of 8 slots, 2-3 per SM - measured, three
+// sweep warps interleave on an SM at no cost), else 32 (3D: staging and store of one CTA overlap
+// the sweeps of the others).
 //
 // Staging: y/z lines (slots contiguous at a fixed element) by 16-byte cp.async; x lines (each line
 // contiguous) by one bulk copy per line (cp.async.bulk + mbarrier, TMA unit), line-major in shared
