@@ -195,7 +195,13 @@ def make_problem(cfg: dict):
     Returns dict(patches=[(cell, ctrl)], u0=[per-patch array (m^dim, ncomp)]).
     Values at Dirichlet control points are returned too; consumers drop them."""
     dim, p, n = cfg["dim"], cfg["p"], cfg["n"]
-    if cfg.get("lshape"):
+    if cfg.get("cells"):
+        # block-structured multi-patch domain: unit cells of the coarse patch grid (any dimension),
+        # one PCG64 stream perturbs the interior points of the patches in the listed order
+        rng = np.random.default_rng(cfg["seed"])
+        patches = [(tuple(c), control_net(dim, p, n, noise=cfg["noise"], origin=tuple(c), rng=rng))
+                   for c in cfg["cells"]]
+    elif cfg.get("lshape"):
         patches = lshape_patches(p, n, cfg["noise"], cfg["seed"])
     elif cfg.get("fan"):
         patches = fan_patches(dim, p, n, cfg["fan"], cfg["noise"], cfg["seed"])
