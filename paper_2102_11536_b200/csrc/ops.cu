@@ -832,7 +832,11 @@ void launch_precond(const PrecArgs& a, cudaStream_t s) {
     if (ok) return;
   }
   // general path (multi-patch / very long lines)
-  const bool batched = !single && !stream;
+  // boxes of a multi-patch problem: every patch in one launch per direction (chunked tiles for few
+  // lines; the whole-line solver also for many lines, 3D boxes)
+  bool seq_multi = !single && stream && (line_mode == 0 || line_mode == 4);
+  for (int d = 0; d < g.dim && seq_multi; ++d) seq_multi = launch_line_seq_multi(a, d, s, true);
+  const bool batched = !single && (!stream || seq_multi);
   if (batched && a.nvec * g.npts * a.kk < (1LL << 31)) {
     // batched Schwarz: prologue + gather in one pass, then one tile launch per direction
     const unsigned int nbg = (unsigned int)((a.nvec * g.npts + NTHREADS - 1) / NTHREADS);
